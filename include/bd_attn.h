@@ -1,0 +1,169 @@
+/* bd_attn.h -- C ABI of the B200 (sm_100a) block-diffusion training hot path
+ * of DiRL / DiPO (arXiv 2512.22234).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n.
+ *
+ * The hot path:
+ *   bd_attn_fwd   -- masked attention over the packed [x0 | xt] sequence with
+ *                    the block-diffusion mask (Eq. 2, Fig. 4,
+ *                    P:261 "repeats both parts blockwise"), fp32 LSE out.
+ *   bd_attn_bwd   -- dQ / dK / dV of the same op, reusing the tile map.
+ *   bd_logprob    -- per-token log-softmax gather (numerators of Eqs. 6-8,
+ *                    P:150-156; CE of Eq. 3), optionally fused with its
+ *                    gradient.
+ *   bd_dipo_*     -- DiPO advantage / token-level reduction at the
+ *                    stop-gradient behaviour policy (P:92, P:172-174,
+ *                    P:179-225); the only cross-GPU step is a NCCL all-reduce
+ *                    of its scalar partials, done by the caller.
+ *
+ * General conventions
+ *  - Every pointer argument is a DEVICE pointer unless marked "host".  The
+ *    library allocates nothing: the caller owns every buffer, including the
+ *    workspace.  Work is enqueued asynchronously on `stream` (a cudaStream_t;
+ *    NULL = legacy default stream).
+ *  - Return value: BD_OK (0) or one of the BD_ERR_* codes below; no
+ *    exception ever crosses the ABI.  bd_error_string() names a code,
+ *    bd_last_error() returns a thread-local message for the last failure.
+ *  - Tensors are dense row-major (C order) with the stated shapes.
+ *  - Device pointers passed to TMA-loaded tensors must be 16-byte aligned.
+ */
+#ifndef BD_ATTN_H_
+#define BD_ATTN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  BD_OK = 0,
+  BD_ERR_INVALID_ARG = 1, /* null pointer, non-positive dimension, Hq % Hkv != 0 */
+  BD_ERR_LAYOUT = 2,      /* L % block_size != 0 ("length not multiple of B -> layout error") */
+  BD_ERR_UNSUPPORTED = 3, /* head_dim not in {64, 128}, sizes beyond int32 tile indexing */
+  BD_ERR_ALIGNMENT = 4,   /* device pointer not 16-byte aligned */
+  BD_ERR_WORKSPACE = 5,   /* workspace null or smaller than bd_attn_workspace_bytes() */
+  BD_ERR_CUDA = 6         /* a CUDA runtime/driver call failed (see bd_last_error) */
+};
+
+/* One block-diffusion attention problem.  Fields follow the paper's statement
+ * of the problem: prompt ("input") length P, response ("output") length R,
+ * block size B ("each block contains B tokens", "input length
+ * 1024 and output length 8192"), GQA heads and head_dim.
+ *
+ * Packed sequence (reading c1): per sequence the token axis holds
+ * Ntot = L + (L - xb) rows, L = P + R:
+ *     rows [0, L)       x0: clean copy of clean positions 0..L-1
+ *     rows [L, Ntot)    xt: noisy copy of clean positions xb..L-1
+ * with xb = 0 if repeat_prompt (DiRL, Fig. 4b; the default) and
+ * xb = P otherwise (TraceRL, Fig. 4a).  Noisy rows keep their clean
+ * position ids (RoPE is the caller's).
+ *
+ * Visibility (blk(p) = p / B):  x0->x0 blk(k) <= blk(q);  xt->x0 blk(k) <
+ * blk(q);  xt->xt blk(k) == blk(q);  x0->xt never.                         */
+typedef struct bd_problem {
+  int32_t batch;
+  int32_t prompt_len;    /* P >= 0                                     */
+  int32_t response_len;  /* R >= 0, L = P + R > 0, L % block_size == 0 */
+  int32_t block_size;    /* B >= 1                                     */
+  int32_t n_q_heads;     /* Hq                                         */
+  int32_t n_kv_heads;    /* Hkv, Hq % Hkv == 0; kv(h) = h / (Hq/Hkv)   */
+  int32_t head_dim;      /* d in {64, 128}                             */
+  int32_t repeat_prompt; /* 1 = DiRL (default), 0 = response-only       */
+  float softmax_scale;   /* <= 0 -> 1/sqrt(head_dim)            */
+} bd_problem;
+
+/* Packed length Ntot of one sequence, or -1 if the problem is invalid. */
+int64_t bd_packed_len(const bd_problem* prob);
+
+/* Workspace bytes needed by bd_attn_fwd (backward = 0) or bd_attn_bwd
+ * (backward = 1).  The forward workspace holds the tile map; the backward
+ * one additionally holds D = rowsum(dO * O) [b, Hq, Ntot] fp32 and the fp32
+ * dQ accumulator [b, Ntot, Hq, d].  Returns 0 for an invalid problem. */
+size_t bd_attn_workspace_bytes(const bd_problem* prob, int backward);
+
+/* Forward.
+ *   q    bf16 [b, Ntot, Hq,  d]      k, v  bf16 [b, Ntot, Hkv, d]
+ *   o    bf16 [b, Ntot, Hq,  d]      (written)
+ *   lse  fp32 [b, Hq, Ntot]          natural-log log-sum-exp of the scaled,
+ *                                    masked scores of each row (written)
+ *   ws   device workspace of >= bd_attn_workspace_bytes(prob, 0) bytes.
+ * O_i = sum_j softmax_j(scale q_i.k_j | M_ij) v_j.  Tiles of 128x128
+ * that the mask leaves empty are never loaded ("accepts fine-grained
+ * masks"; S:97 block skip).  Deterministic. */
+int bd_attn_fwd(const bd_problem* prob, const void* q, const void* k, const void* v, void* o, float* lse,
+                void* ws, size_t ws_bytes, void* stream);
+
+/* Backward of bd_attn_fwd for upstream gradient dout (bf16, like q), given the
+ * forward's o and lse.  Writes dq (bf16 like q) and dk, dv (bf16 like k); dk
+ * and dv sum over the Hq/Hkv query heads of each kv head.  ws must be
+ * >= bd_attn_workspace_bytes(prob, 1) bytes.  The dQ reduction order is not
+ * deterministic (fp32 atomics). */
+int bd_attn_bwd(const bd_problem* prob, const void* q, const void* k, const void* v, const void* o,
+                const float* lse, const void* dout, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
+                void* stream);
+
+/* Per-token log-probabilities over a vocabulary.
+ *   logits   bf16 [n_rows, vocab] with row stride `row_stride` elements
+ *   targets  int32 [n_rows]
+ *   logp     fp32 [n_rows]  logp_n = z[n, t_n] - LSE_n        (written)
+ *   lse      fp32 [n_rows]  LSE_n = ln sum_v exp z[n, v]      (written; may be NULL)
+ *   dlogp    fp32 [n_rows]  upstream gradient w_n, or NULL for forward only
+ *   dlogits  bf16 [n_rows, vocab] (row stride dlogits_stride) receiving
+ *            w_n (1[v = t_n] - softmax(z_n)_v); may alias logits (in place,
+ *            then dlogits_stride must equal row_stride); ignored if dlogp is NULL.
+ * A target outside [0, vocab) yields logp = NaN for that row (the DiPO step
+ * treats a non-finite value as "abort"). */
+int bd_logprob(int64_t n_rows, int32_t vocab, const void* logits, int64_t row_stride, const int32_t* targets,
+               float* logp, float* lse, const float* dlogp, void* dlogits, int64_t dlogits_stride, void* stream);
+
+/* DiPO, step 1: per-group partial statistics of the local trajectories.
+ *   rewards        fp32 [n_traj]       r_i
+ *   group_of_traj  int32 [n_traj]      global group id in [0, n_groups)
+ *   traj_len       int32 [n_traj]      |tau_i| in tokens (reading c10)
+ *   group_stats    fp64 [n_groups, 3]  += (sum r, count, sum |tau|)   (accumulated;
+ *                                      zero it first; all-reduce(SUM) it across
+ *                                      ranks when a group straddles ranks)  */
+int bd_dipo_group_stats(int32_t n_traj, const float* rewards, const int32_t* group_of_traj,
+                        const int32_t* traj_len, int32_t n_groups, double* group_stats, void* stream);
+
+/* DiPO, step 2: token-level objective of Eq. 8 with the
+ * stop-gradient behaviour policy of Eq. 7.
+ *   logp, logp_old fp32 [n_tokens]    rho_k = exp(logp_k - logp_old_k)
+ *   traj_of_token  int32 [n_tokens]    local trajectory index
+ *   rewards, group_of_traj             as in step 1 (local trajectories)
+ *   group_stats    fp64 [n_groups, 3]  globally reduced output of step 1
+ *   n_groups_global                    number of non-empty groups overall
+ *   eps                                clip range of C_eps
+ *   dlogp          fp32 [n_tokens]     dloss/dlogp_k (written)
+ *   partials       fp64 [3]            += (loss partial, tokens, clipped tokens)
+ * A_i = r_i - mean_g r;  loss = -(1/n_groups) sum_g (1/N_g) sum C_eps(rho, A). */
+int bd_dipo_token_loss(int64_t n_tokens, const float* logp, const float* logp_old, const int32_t* traj_of_token,
+                       const float* rewards, const int32_t* group_of_traj, const double* group_stats,
+                       int32_t n_groups_global, float eps, float* dlogp, double* partials, void* stream);
+
+/* Tile map (host path, for tests).  Writes the ordered list of non-empty
+ * 128x128 tiles as 5-tuples (q_seg, q_tile, k_seg, k_tile, kind) of int32
+ * into host_out (capacity `cap` int32 elements), kind 1 = FULL, 2 = PARTIAL;
+ * segment 0 = x0, 1 = xt; tiles in packed order.  *n_tiles (host) receives
+ * the number of tuples.  Returns BD_ERR_WORKSPACE if cap is too small. */
+int bd_tilemap_dump(const bd_problem* prob, int32_t* host_out, size_t cap, int64_t* n_tiles);
+
+/* Tile-map statistics (host): counts of q-tiles, non-empty, FULL and PARTIAL
+ * tiles per (sequence, head); out = int64[4]. */
+int bd_tilemap_stats(const bd_problem* prob, int64_t* out);
+
+const char* bd_error_string(int code);
+const char* bd_last_error(void);
+
+/* Hardware self-test of the UMMA / TMEM / TMA conventions (diagnostic).
+ * a, b, v bf16 [128][128]; c = a.b^T, o_* = bf16(c).v via TMEM-A, smem-A
+ * (K-major) and smem-A (MN-major); all fp32 [128][128]. */
+int bd_selftest_mma(const void* a, const void* b, const void* v, float* c, float* o_ts, float* o_ss, float* o_mn,
+                    void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BD_ATTN_H_ */

@@ -1,0 +1,39 @@
+// Error reporting shared by every C-ABI entry point.
+#include "abi_common.h"
+
+#include <cstdio>
+#include <cstdarg>
+
+namespace bd {
+
+static thread_local char g_last_error[512] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return BD_OK;
+  return set_error(BD_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+}  // namespace bd
+
+extern "C" const char* bd_error_string(int code) {
+  switch (code) {
+    case BD_OK: return "BD_OK";
+    case BD_ERR_INVALID_ARG: return "BD_ERR_INVALID_ARG";
+    case BD_ERR_LAYOUT: return "BD_ERR_LAYOUT";
+    case BD_ERR_UNSUPPORTED: return "BD_ERR_UNSUPPORTED";
+    case BD_ERR_ALIGNMENT: return "BD_ERR_ALIGNMENT";
+    case BD_ERR_WORKSPACE: return "BD_ERR_WORKSPACE";
+    case BD_ERR_CUDA: return "BD_ERR_CUDA";
+    default: return "BD_ERR_UNKNOWN";
+  }
+}
+
+extern "C" const char* bd_last_error(void) { return bd::g_last_error; }

@@ -1,0 +1,14 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "bd_attn.h"
+
+namespace bd {
+
+int set_error(int code, const char* fmt, ...);
+int check_cuda(cudaError_t e, const char* what);
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace bd

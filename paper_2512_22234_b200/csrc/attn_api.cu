@@ -1,0 +1,71 @@
+// C ABI of the attention path: validation, workspace carving, launches.
+#include "abi_common.h"
+#include "problem.h"
+#include "attn_common.h"
+
+namespace bd {
+namespace {
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct WsLayout {
+  size_t map_off, dsum_off, dq_off, total;
+};
+
+WsLayout ws_layout(const bd_problem& p, int backward) {
+  const Geom g = geom_of(p);
+  WsLayout w{};
+  w.map_off = 0;
+  size_t off = align256((size_t)map_words(g) * sizeof(int));
+  if (backward) {
+    w.dsum_off = off;
+    off = align256(off + (size_t)p.batch * p.n_q_heads * g.N * sizeof(float));
+    w.dq_off = off;
+    off = align256(off + (size_t)p.batch * g.N * p.n_q_heads * p.head_dim * sizeof(float));
+  }
+  w.total = off;
+  return w;
+}
+
+int check_ptrs(std::initializer_list<const void*> ps) {
+  for (const void* x : ps) {
+    if (!x) return set_error(BD_ERR_INVALID_ARG, "null tensor pointer");
+    if (!aligned16(x)) return set_error(BD_ERR_ALIGNMENT, "tensor pointer not 16-byte aligned");
+  }
+  return BD_OK;
+}
+
+int check_head_dim(const bd_problem& p) {
+  if (p.head_dim != 64 && p.head_dim != 128)
+    return set_error(BD_ERR_UNSUPPORTED, "head_dim %d not in {64, 128}", p.head_dim);
+  return BD_OK;
+}
+
+}  // namespace
+}  // namespace bd
+
+extern "C" int64_t bd_packed_len(const bd_problem* prob) {
+  if (bd::validate_problem(prob)) return -1;
+  return bd::geom_of(*prob).N;
+}
+
+extern "C" size_t bd_attn_workspace_bytes(const bd_problem* prob, int backward) {
+  if (bd::validate_problem(prob)) return 0;
+  return bd::ws_layout(*prob, backward).total;
+}
+
+extern "C" int bd_attn_fwd(const bd_problem* prob, const void* q, const void* k, const void* v, void* o, float* lse,
+                           void* ws, size_t ws_bytes, void* stream_) {
+  using namespace bd;
+  int rc = validate_problem(prob);
+  if (rc) return rc;
+  if ((rc = check_head_dim(*prob))) return rc;
+  if ((rc = check_ptrs({q, k, v, o, lse, ws}))) return rc;
+  const WsLayout wl = ws_layout(*prob, 0);
+  if (ws_bytes < wl.total) return set_error(BD_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, wl.total);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const Geom g = geom_of(*prob);
+  int* map = reinterpret_cast<int*>(static_cast<char*>(ws) + wl.map_off);
+  if ((rc = build_map_device(g, map, stream))) return rc;
+  return run_attn_fwd(*prob, g, q, k, v, o, lse, map, stream);
+}

@@ -1,0 +1,27 @@
+// Shared host helpers for the attention kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "tma_host.h"
+#include "tilemap.cuh"
+#include "bd_attn.h"
+
+namespace bd {
+
+// 4-D TMA map over a [b, N, H, D] bf16 tensor: dims (D, H, N, b), box
+// (64, 1, 128, 1), 128-byte swizzle.  Rows past N are zero-filled.
+inline bool make_qkv_tmap(CUtensorMap* m, const void* base, int batch, int N, int H, int D) {
+  const uint64_t dims[4] = {(uint64_t)D, (uint64_t)H, (uint64_t)N, (uint64_t)batch};
+  const uint64_t strides[3] = {(uint64_t)D * 2, (uint64_t)H * D * 2, (uint64_t)N * H * D * 2};
+  const uint32_t box[4] = {64, 1, 128, 1};
+  return make_tmap_bf16(m, base, 4, dims, strides, box);
+}
+
+int build_map_device(const Geom& g, int* ws, cudaStream_t stream);
+int run_attn_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, void* o,
+                 float* lse, const int* map, cudaStream_t stream);
+int run_attn_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, const void* o,
+                 const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, float* dsum,
+                 float* dq_acc, cudaStream_t stream);
+
+}  // namespace bd

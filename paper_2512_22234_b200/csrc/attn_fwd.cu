@@ -1,0 +1,348 @@
+// bd_attn_fwd: block-diffusion masked attention forward, sm_100a.
+//
+// Computes, for every packed query row i of every (sequence, q-head),
+//   O_i = sum_j softmax_j(scale q_i.k_j | M_ij) v_j,  LSE_i = ln sum_j exp(scale q_i.k_j | M_ij)
+// with M the DiRL block-diffusion mask (Eq. 2).
+//
+// Design:
+//  * One CTA per (q-tile, sequence, pair of q-heads of one kv group): the two
+//    query tiles share every K/V tile (GQA packing), so each K/V tile loaded by
+//    TMA feeds two S = QK^T and two O += PV tcgen05 MMAs.  When Hq/Hkv is odd
+//    a CTA carries one q-head (NQ = 1) and two CTAs share an SM.
+//  * Only the k-tiles listed by the tile map for this q-tile are visited
+//    (EMPTY tiles are never loaded); the list is LPT-ordered across CTAs.
+//  * Warp roles: warps [0, 4 NQ) are softmax warpgroups (one per q-tile, a
+//    thread owns one row = one TMEM lane), warp 4 NQ issues TMA, warp 4 NQ + 1
+//    issues tcgen05.mma.  S and O accumulate in TMEM (S_q at column 128 q,
+//    O_q after the S regions); P (bf16) overwrites S_q in place and feeds the
+//    PV MMA straight from TMEM.
+//  * Online softmax in the exp2 domain with lazy rescaling: the running max is
+//    only raised when a tile's max exceeds it by > 8 (factor 256), so the O
+//    correction (TMEM ld/mul/st) is rare.
+//  * Mask: on PARTIAL or ragged tiles each row keeps the columns inside its
+//    visible interval (tilemap.cuh row_interval); FULL tiles are unmasked.
+#include "sm100.cuh"
+#include "tma_host.h"
+#include "tilemap.cuh"
+#include "problem.h"
+#include "attn_common.h"
+
+#include <cuda_bf16.h>
+
+namespace bd {
+namespace {
+
+template <int D, int NQ>
+struct FwdCfg {
+  static constexpr int kTileBytes = 128 * D * 2;
+  static constexpr int kStages = NQ == 2 ? 4 : 2;
+  static constexpr int kSoftmaxWarps = 4 * NQ;
+  static constexpr int kTmaWarp = kSoftmaxWarps;
+  static constexpr int kMmaWarp = kSoftmaxWarps + 1;
+  static constexpr int kThreads = (kSoftmaxWarps + 2) * 32;
+  static constexpr int kSCol = 0;                 // S_q at 128 q
+  static constexpr int kOCol = 128 * NQ;          // O_q at kOCol + D q
+  static constexpr int kTmemUsed = 128 * NQ + D * NQ;
+  static constexpr uint32_t kTmemCols = kTmemUsed <= 256 ? 256 : 512;
+  // barriers: q_full, kv_full[S], kv_empty[S], s_full[NQ], p_full[NQ], pv_done[NQ]
+  static constexpr int kNumBars = 1 + 2 * kStages + 3 * NQ;
+  static constexpr int kSmemBytes = NQ * kTileBytes + kStages * kTileBytes + kNumBars * 8 + 16 + 1024;
+};
+
+struct FwdArgs {
+  const int* map;
+  __nv_bfloat16* o;
+  float* lse;
+  int batch, n_q_heads, n_hg, group, N;
+  Geom g;
+  float scale_log2;
+};
+
+template <int D, int NQ>
+__global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const FwdArgs a) {
+  using C = FwdCfg<D, NQ>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + NQ * C::kTileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kStages * C::kTileBytes);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + C::kStages;
+  uint64_t* s_full = kv_empty + C::kStages;
+  uint64_t* p_full = s_full + NQ;
+  uint64_t* pv_done = p_full + NQ;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
+
+  const int warp = (int)warp_id(), lane = (int)lane_id();
+  const Geom& g = a.g;
+
+  // ---- work unit: LPT rank of the q-tile, then (sequence, head pair)
+  const int per_tile = a.batch * a.n_hg;
+  const int rank = blockIdx.x / per_tile;
+  const int rem = blockIdx.x - rank * per_tile;
+  const int b = rem / a.n_hg;
+  const int h0 = (rem - b * a.n_hg) * NQ;
+  const int kvh = h0 / a.group;
+  const MapView mv{const_cast<int*>(a.map), g.NT, map_capacity(g)};
+  const int qt = mv.fwd_order()[rank];
+  const int e0 = mv.row_ptr()[qt];
+  const int n_kt = mv.row_ptr()[qt + 1] - e0;
+  const int* ents = mv.row_ent() + e0;
+  const int q0 = tile_start(g, qt), q1 = tile_end(g, qt), qseg = tile_seg(g, qt);
+
+  if (warp == 0) tmem_alloc<C::kTmemCols>(tslot);
+  if (warp == C::kTmaWarp && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int q = 0; q < NQ; ++q) {
+      mbar_init(&s_full[q], 1);
+      mbar_init(&p_full[q], 4);
+      mbar_init(&pv_done[q], 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == C::kTmaWarp) {
+    // ================================================================ TMA
+    if (elect_one()) {
+      mbar_expect_tx(q_full, NQ * C::kTileBytes);
+      for (int q = 0; q < NQ; ++q)
+        for (int kb = 0; kb < D / 64; ++kb)
+          tma_load_4d(sQ + q * C::kTileBytes + kb * 16384, &tmQ, q_full, kb * 64, h0 + q, q0, b);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int j = 0; j < n_kt; ++j) {
+        const int k0 = tile_start(g, entry_tile(ents[j]));
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv) {
+          mbar_wait(&kv_empty[stage], phase ^ 1);
+          mbar_expect_tx(&kv_full[stage], C::kTileBytes);
+          uint8_t* dst = sKV + stage * C::kTileBytes;
+          for (int kb = 0; kb < D / 64; ++kb)
+            tma_load_4d(dst + kb * 16384, kv ? &tmV : &tmK, &kv_full[stage], kb * 64, kvh, k0, b);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == C::kMmaWarp) {
+    // ================================================================ MMA
+    if (elect_one()) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int j = 0; j < n_kt; ++j) {
+        const int sK = stage;
+        const uint32_t phK = phase;
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        const int sV = stage;
+        const uint32_t phV = phase;
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        // ---- S_q = Q_q K^T
+        mbar_wait(&kv_full[sK], phK);
+        tc_fence_after();
+        const uint32_t kaddr = smem_u32(sKV + sK * C::kTileBytes);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          if (j > 0) {
+            mbar_wait(&pv_done[q], (j - 1) & 1);  // P_q(j-1) (aliasing S_q) consumed
+            tc_fence_after();
+          }
+          const uint32_t qaddr = smem_u32(sQ + q * C::kTileBytes);
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+            umma_ss(tbase + C::kSCol + 128 * q, umma_desc_sw128(qaddr + off, 16, 1024),
+                    umma_desc_sw128(kaddr + off, 16, 1024), idesc_s, k > 0);
+          }
+          umma_commit(&s_full[q]);
+        }
+        umma_commit(&kv_empty[sK]);
+        // ---- O_q += P_q V
+        mbar_wait(&kv_full[sV], phV);
+        tc_fence_after();
+        const uint32_t vaddr = smem_u32(sKV + sV * C::kTileBytes);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          mbar_wait(&p_full[q], j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            umma_ts(tbase + C::kOCol + D * q, tbase + C::kSCol + 128 * q + k * 8,
+                    umma_desc_sw128(vaddr + k * 2048, 16384, 1024), idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&pv_done[q]);
+        }
+        umma_commit(&kv_empty[sV]);
+      }
+    }
+  } else {
+    // ============================================================ softmax
+    const int q = warp >> 2;
+    const int r = (warp & 3) * 32 + lane;  // row within the tile == TMEM lane
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS = tbase + lane_off + C::kSCol + 128 * q;
+    const uint32_t tO = tbase + lane_off + C::kOCol + D * q;
+    const int row = q0 + r;
+    int lo0, hi0, lo1, hi1;
+    row_interval(g, qseg, row, 0, lo0, hi0);
+    row_interval(g, qseg, row, 1, lo1, hi1);
+    const float sl2 = a.scale_log2;
+    float m = -INFINITY, l = 0.f;
+
+    for (int j = 0; j < n_kt; ++j) {
+      const int ent = ents[j];
+      const int kt = entry_tile(ent);
+      const int k0 = tile_start(g, kt), k1 = tile_end(g, kt);
+      const bool need_mask = entry_kind(ent) == kKindPartial || (k1 - k0) < 128;
+      mbar_wait(&s_full[q], j & 1);
+      tc_fence_after();
+      uint32_t sr[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tS + 32 * c, sr + 32 * c);
+      tmem_ld_wait();
+      float* s = reinterpret_cast<float*>(sr);
+      if (need_mask) {
+        const bool xt = tile_seg(g, kt) != 0;
+        const int lo = (xt ? lo1 : lo0) - k0;
+        const int hi = min(xt ? hi1 : hi0, k1) - k0;
+#pragma unroll
+        for (int c = 0; c < 128; ++c) s[c] = (c >= lo && c < hi) ? s[c] : -INFINITY;
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
+      const float tmax = mx * sl2;
+      float m_new = m;
+      bool resc = false;
+      if (tmax > m + 8.f) {
+        m_new = tmax;
+        resc = true;
+      }
+      const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+      const float alpha = resc ? ex2_approx(m - m_use) : 1.f;
+      float sum = 0.f;
+      uint32_t pk[64];
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        const float p0 = ex2_approx(fmaf(s[2 * c], sl2, -m_use));
+        const float p1 = ex2_approx(fmaf(s[2 * c + 1], sl2, -m_use));
+        sum += p0 + p1;
+        pk[c] = pack_bf16x2(p0, p1);
+      }
+      l = l * alpha + sum;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) tmem_st32(tS + 32 * c, pk + 32 * c);
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
+        // O_q *= alpha (PV(j-1) has completed: S_q(j) was issued after it)
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t ov[32];
+          tmem_ld32(tO + 32 * c, ov);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+          tmem_st32(tO + 32 * c, ov);
+        }
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[q]);
+      m = m_new;
+    }
+    // ---- epilogue
+    mbar_wait(&pv_done[q], (n_kt - 1) & 1);
+    tc_fence_after();
+    const int h = h0 + q;
+    const bool valid = row < q1;
+    const float inv_l = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* orow = a.o + (((size_t)b * a.N + row) * a.n_q_heads + h) * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t ov[32];
+      tmem_ld32(tO + 32 * c, ov);
+      tmem_ld_wait();
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        pk[i] = pack_bf16x2(__uint_as_float(ov[2 * i]) * inv_l, __uint_as_float(ov[2 * i + 1]) * inv_l);
+      if (valid) {
+        uint4* dst = reinterpret_cast<uint4*>(orow + 32 * c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      }
+    }
+    if (valid) {
+      const float m_use = (m == -INFINITY) ? 0.f : m;
+      a.lse[((size_t)b * a.n_q_heads + h) * a.N + row] =
+          l > 0.f ? (m_use + __log2f(l)) * 0.69314718055994531f : -INFINITY;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<C::kTmemCols>(tbase);
+}
+
+template <int D, int NQ>
+int launch_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, void* o,
+               float* lse, const int* map, cudaStream_t stream) {
+  using C = FwdCfg<D, NQ>;
+  CUtensorMap tmQ, tmK, tmV;
+  if (!make_qkv_tmap(&tmQ, q, p.batch, g.N, p.n_q_heads, D) || !make_qkv_tmap(&tmK, k, p.batch, g.N, p.n_kv_heads, D) ||
+      !make_qkv_tmap(&tmV, v, p.batch, g.N, p.n_kv_heads, D))
+    return set_error(BD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::kSmemBytes);
+    if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(fwd)");
+    attr = true;
+  }
+  FwdArgs a;
+  a.map = map;
+  a.o = reinterpret_cast<__nv_bfloat16*>(o);
+  a.lse = lse;
+  a.batch = p.batch;
+  a.n_q_heads = p.n_q_heads;
+  a.n_hg = p.n_q_heads / NQ;
+  a.group = p.n_q_heads / p.n_kv_heads;
+  a.N = g.N;
+  a.g = g;
+  a.scale_log2 = scale_of(p) * 1.4426950408889634f;
+  const long long grid = (long long)g.NT * p.batch * a.n_hg;
+  if (grid > 0x7FFFFFFF) return set_error(BD_ERR_UNSUPPORTED, "grid too large");
+  attn_fwd_kernel<D, NQ><<<(unsigned)grid, C::kThreads, C::kSmemBytes, stream>>>(tmQ, tmK, tmV, a);
+  return check_cuda(cudaGetLastError(), "attn_fwd_kernel launch");
+}
+
+}  // namespace
+
+int run_attn_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, void* o,
+                 float* lse, const int* map, cudaStream_t stream) {
+  const bool pair = (p.n_q_heads / p.n_kv_heads) % 2 == 0;
+  if (p.head_dim == 128) return pair ? launch_fwd<128, 2>(p, g, q, k, v, o, lse, map, stream)
+                                     : launch_fwd<128, 1>(p, g, q, k, v, o, lse, map, stream);
+  if (p.head_dim == 64) return pair ? launch_fwd<64, 2>(p, g, q, k, v, o, lse, map, stream)
+                                    : launch_fwd<64, 1>(p, g, q, k, v, o, lse, map, stream);
+  return set_error(BD_ERR_UNSUPPORTED, "head_dim %d not in {64, 128}", p.head_dim);
+}
+
+}  // namespace bd

@@ -1,0 +1,40 @@
+// Validation of bd_problem and derived geometry (host).
+#pragma once
+#include <cmath>
+#include <cstdint>
+
+#include "abi_common.h"
+#include "tilemap.cuh"
+
+namespace bd {
+
+constexpr int kMaxTiles = 8192;  // NT bound of the device map builder (L <= ~512K)
+
+inline int validate_problem(const bd_problem* p) {
+  if (!p) return set_error(BD_ERR_INVALID_ARG, "problem is null");
+  if (p->batch <= 0 || p->block_size <= 0 || p->n_q_heads <= 0 || p->n_kv_heads <= 0 || p->head_dim <= 0)
+    return set_error(BD_ERR_INVALID_ARG, "non-positive dimension");
+  if (p->prompt_len < 0 || p->response_len < 0)
+    return set_error(BD_ERR_INVALID_ARG, "negative length");
+  const int64_t L = (int64_t)p->prompt_len + p->response_len;
+  if (L <= 0) return set_error(BD_ERR_INVALID_ARG, "empty sequence");
+  if (p->n_q_heads % p->n_kv_heads) return set_error(BD_ERR_INVALID_ARG, "n_q_heads %% n_kv_heads != 0");
+  if (L % p->block_size) return set_error(BD_ERR_LAYOUT, "L = %lld not a multiple of block_size %d", (long long)L,
+                                          p->block_size);
+  if (p->repeat_prompt != 0 && p->repeat_prompt != 1) return set_error(BD_ERR_INVALID_ARG, "repeat_prompt not 0/1");
+  if (2 * L > (int64_t)1 << 30) return set_error(BD_ERR_UNSUPPORTED, "sequence too long");
+  const int T = (int)((L + kTileRows - 1) / kTileRows);
+  if (2 * T > kMaxTiles) return set_error(BD_ERR_UNSUPPORTED, "sequence too long for the tile map");
+  return BD_OK;
+}
+
+inline Geom geom_of(const bd_problem& p) {
+  const int L = p.prompt_len + p.response_len;
+  return make_geom(L, p.repeat_prompt ? 0 : p.prompt_len, p.block_size);
+}
+
+inline float scale_of(const bd_problem& p) {
+  return p.softmax_scale > 0.f ? p.softmax_scale : 1.0f / std::sqrt((float)p.head_dim);
+}
+
+}  // namespace bd

@@ -1,0 +1,154 @@
+// Block-diffusion mask -> 128x128 tile map (block-sparse schedule).
+//
+// The mask rule (Eq. 2; Fig. 4b) makes every
+// query row's visible keys, per key segment, ONE contiguous packed interval:
+//   x0 row at clean position p, bq = p / B:
+//       x0 keys [0, min((bq+1)B, L))                (block-causal)
+//   xt row at clean position p:
+//       x0 keys [0, bq B)                            (clean blocks < bq)
+//       xt keys clean positions [max(bq B, xb), min((bq+1)B, L))   (own block)
+// Both ends are non-decreasing in p.  The builder below classifies every
+// (q-tile, k-tile) pair from these intervals (FULL / PARTIAL / EMPTY), and
+// the kernels evaluate the same intervals per row on PARTIAL tiles.  EMPTY
+// tiles are never listed, hence never loaded.
+//
+// One __host__ __device__ implementation serves the device builder kernel
+// (bd_attn_fwd/bwd build the map into the caller's workspace every call) and
+// the host path (bd_tilemap_dump / bd_tilemap_stats).
+#pragma once
+#include <cstdint>
+
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#endif
+
+namespace bd {
+
+constexpr int kTileRows = 128;
+constexpr int kKindFull = 1;
+constexpr int kKindPartial = 2;
+
+struct Geom {
+  int L, xb, N, B, T0, T1, NT;
+};
+
+__host__ __device__ inline Geom make_geom(int L, int xb, int B) {
+  Geom g;
+  g.L = L;
+  g.xb = xb;
+  g.N = L + (L - xb);
+  g.B = B;
+  g.T0 = (L + kTileRows - 1) / kTileRows;
+  g.T1 = (L - xb + kTileRows - 1) / kTileRows;
+  g.NT = g.T0 + g.T1;
+  return g;
+}
+
+__host__ __device__ inline int tile_seg(const Geom& g, int t) { return t >= g.T0 ? 1 : 0; }
+__host__ __device__ inline int tile_idx(const Geom& g, int t) { return t >= g.T0 ? t - g.T0 : t; }
+__host__ __device__ inline int tile_start(const Geom& g, int t) {
+  return t >= g.T0 ? g.L + (t - g.T0) * kTileRows : t * kTileRows;
+}
+__host__ __device__ inline int tile_end(const Geom& g, int t) {
+  const int s = tile_start(g, t) + kTileRows;
+  const int e = t >= g.T0 ? g.N : g.L;
+  return s < e ? s : e;
+}
+
+// Visible packed-column interval [lo, hi) of packed row `row` (a row of
+// segment `qseg`) within key segment `kseg`.  Empty intervals have lo >= hi.
+__host__ __device__ inline void row_interval(const Geom& g, int qseg, int row, int kseg, int& lo, int& hi) {
+  const int p = qseg ? g.xb + (row - g.L) : row;  // clean position
+  const int bq = p / g.B;
+  const int b0 = bq * g.B, b1 = b0 + g.B;
+  if (kseg == 0) {
+    lo = 0;
+    hi = qseg ? b0 : (b1 < g.L ? b1 : g.L);
+  } else if (qseg == 0) {
+    lo = hi = g.L;  // x0 never sees xt
+  } else {
+    const int a = b0 > g.xb ? b0 : g.xb;
+    const int c = b1 < g.L ? b1 : g.L;
+    lo = g.L + a - g.xb;
+    hi = g.L + c - g.xb;
+  }
+}
+
+// Kind of tile pair (qt, kt): 0 = EMPTY, kKindFull, kKindPartial -- decided
+// over the tile's valid rows and columns, row by row.
+__host__ __device__ inline int classify_pair(const Geom& g, int qt, int kt) {
+  const int q0 = tile_start(g, qt), q1 = tile_end(g, qt), qs = tile_seg(g, qt);
+  const int k0 = tile_start(g, kt), k1 = tile_end(g, kt), ks = tile_seg(g, kt);
+  bool any = false, all = true;
+  for (int r = q0; r < q1; ++r) {
+    int lo, hi;
+    row_interval(g, qs, r, ks, lo, hi);
+    const int a = lo > k0 ? lo : k0;
+    const int b = hi < k1 ? hi : k1;
+    if (b > a) any = true;
+    if (!(a == k0 && b == k1)) all = false;
+  }
+  return any ? (all ? kKindFull : kKindPartial) : 0;
+}
+
+// Candidate k-tiles of q-tile qt: the union of its rows' intervals is
+// [0, hi0) in x0 and [lo1, hi1) in xt (intervals are monotone and the xt ones
+// of consecutive blocks are adjacent), so only tiles overlapping those ranges
+// are classified.
+__host__ __device__ inline void candidate_range(const Geom& g, int qt, int kseg, int& t_lo, int& t_hi) {
+  const int q0 = tile_start(g, qt), q1 = tile_end(g, qt), qs = tile_seg(g, qt);
+  int lo_a, hi_a, lo_b, hi_b;
+  row_interval(g, qs, q0, kseg, lo_a, hi_a);
+  row_interval(g, qs, q1 - 1, kseg, lo_b, hi_b);
+  const int lo = lo_a, hi = hi_b;
+  const int base = kseg ? g.T0 : 0;
+  const int seg0 = kseg ? g.L : 0;
+  if (hi <= lo) {
+    t_lo = t_hi = base;
+    return;
+  }
+  t_lo = base + (lo - seg0) / kTileRows;
+  t_hi = base + (hi - seg0 + kTileRows - 1) / kTileRows;
+}
+
+// Entries are int32: k-tile index | kind << 28.
+__host__ __device__ inline int entry_make(int tile, int kind) { return tile | (kind << 28); }
+__host__ __device__ inline int entry_tile(int e) { return e & 0x0FFFFFFF; }
+__host__ __device__ inline int entry_kind(int e) { return (e >> 28) & 0xF; }
+
+// Workspace image of the map (int32 words):
+//   [0]            magic
+//   [1..7]         L, xb, B, NT, T0, n_entries, max_row_len
+//   row_ptr[NT+1]  entries of q-tile t are row_ent[row_ptr[t] .. row_ptr[t+1])
+//   row_ent[cap]   k-tiles in increasing order
+//   col_ptr[NT+1]  column CSR (q-tiles visiting k-tile t), for the backward
+//   col_ent[cap]   q-tile | kind << 28, q-tiles in increasing order
+//   fwd_order[NT]  q-tiles by decreasing row length (longest first, LPT)
+//   bwd_order[NT]  k-tiles by decreasing column length
+constexpr int kMapMagic = 0x42444D31;  // "BDM1"
+constexpr int kMapHeader = 8;
+
+struct MapView {
+  int* base;
+  int NT, cap;
+  __host__ __device__ int* row_ptr() const { return base + kMapHeader; }
+  __host__ __device__ int* row_ent() const { return row_ptr() + NT + 1; }
+  __host__ __device__ int* col_ptr() const { return row_ent() + cap; }
+  __host__ __device__ int* col_ent() const { return col_ptr() + NT + 1; }
+  __host__ __device__ int* fwd_order() const { return col_ent() + cap; }
+  __host__ __device__ int* bwd_order() const { return fwd_order() + NT; }
+};
+
+// Upper bound on entries: a q-tile lists at most T0 x0 tiles and 2 xt tiles
+// (its own block spans at most two xt tiles when B <= 128; in general
+// ceil(B/128)+1).
+__host__ __device__ inline int map_capacity(const Geom& g) {
+  const int xt_max = (g.B + kTileRows - 1) / kTileRows + 1;
+  return g.NT * (g.T0 + (xt_max < g.T1 ? xt_max : g.T1));
+}
+__host__ __device__ inline long long map_words(const Geom& g) {
+  return (long long)kMapHeader + 2LL * (g.NT + 1) + 2LL * map_capacity(g) + 2LL * g.NT;
+}
+
+}  // namespace bd

@@ -1,0 +1,269 @@
+// Tile-map builder: device kernel (writes the map into the caller's
+// workspace on the call's stream -- no host round trip, no allocation) and
+// the identical host path behind bd_tilemap_dump / bd_tilemap_stats.
+#include "tilemap.cuh"
+#include "abi_common.h"
+#include "problem.h"
+
+#include <algorithm>
+#include <vector>
+
+namespace bd {
+
+// ------------------------------------------------------------------ host
+void build_map_host(const Geom& g, std::vector<int>& w) {
+  const int cap = map_capacity(g);
+  w.assign(static_cast<size_t>(map_words(g)), 0);
+  MapView mv{w.data(), g.NT, cap};
+  w[0] = kMapMagic;
+  w[1] = g.L;
+  w[2] = g.xb;
+  w[3] = g.B;
+  w[4] = g.NT;
+  w[5] = g.T0;
+  int n = 0, maxrow = 0;
+  std::vector<int> rowlen(g.NT), collen(g.NT, 0);
+  for (int t = 0; t < g.NT; ++t) {
+    mv.row_ptr()[t] = n;
+    for (int ks = 0; ks < 2; ++ks) {
+      int a, b;
+      candidate_range(g, t, ks, a, b);
+      for (int kt = a; kt < b; ++kt) {
+        const int kind = classify_pair(g, t, kt);
+        if (kind) {
+          mv.row_ent()[n++] = entry_make(kt, kind);
+          collen[kt]++;
+        }
+      }
+    }
+    rowlen[t] = n - mv.row_ptr()[t];
+    maxrow = std::max(maxrow, rowlen[t]);
+  }
+  mv.row_ptr()[g.NT] = n;
+  w[6] = n;
+  w[7] = maxrow;
+  int c = 0;
+  for (int kt = 0; kt < g.NT; ++kt) {
+    mv.col_ptr()[kt] = c;
+    c += collen[kt];
+  }
+  mv.col_ptr()[g.NT] = c;
+  std::vector<int> fill(g.NT, 0);
+  for (int t = 0; t < g.NT; ++t)
+    for (int e = mv.row_ptr()[t]; e < mv.row_ptr()[t + 1]; ++e) {
+      const int kt = entry_tile(mv.row_ent()[e]);
+      mv.col_ent()[mv.col_ptr()[kt] + fill[kt]++] = entry_make(t, entry_kind(mv.row_ent()[e]));
+    }
+  std::vector<int> ord(g.NT);
+  for (int i = 0; i < g.NT; ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return rowlen[a] > rowlen[b]; });
+  for (int i = 0; i < g.NT; ++i) mv.fwd_order()[i] = ord[i];
+  for (int i = 0; i < g.NT; ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return collen[a] > collen[b]; });
+  for (int i = 0; i < g.NT; ++i) mv.bwd_order()[i] = ord[i];
+}
+
+// ---------------------------------------------------------------- device
+namespace {
+
+constexpr int kBuildThreads = 1024;
+
+// Exclusive scan of cnt[0..n) into out[0..n], out[n] = total.  All threads.
+__device__ void block_exclusive_scan(const int* cnt, int* out, int n, int* scratch) {
+  const int tid = threadIdx.x;
+  const int per = (n + kBuildThreads - 1) / kBuildThreads;
+  const int a = tid * per, b = min(n, a + per);
+  int s = 0;
+  for (int i = a; i < b; ++i) s += cnt[i];
+  scratch[tid] = s;
+  __syncthreads();
+  // Hillis-Steele over the 1024 partials
+  for (int off = 1; off < kBuildThreads; off <<= 1) {
+    const int v = tid >= off ? scratch[tid - off] : 0;
+    __syncthreads();
+    scratch[tid] += v;
+    __syncthreads();
+  }
+  int run = scratch[tid] - s;  // exclusive prefix of this chunk
+  for (int i = a; i < b; ++i) {
+    out[i] = run;
+    run += cnt[i];
+  }
+  if (tid == kBuildThreads - 1) out[n] = scratch[tid];
+  __syncthreads();
+}
+
+// Warp-cooperative classification (same result as classify_pair).
+__device__ int classify_pair_warp(const Geom& g, int qt, int kt) {
+  const int q0 = tile_start(g, qt), q1 = tile_end(g, qt), qs = tile_seg(g, qt);
+  const int k0 = tile_start(g, kt), k1 = tile_end(g, kt), ks = tile_seg(g, kt);
+  bool any = false, all = true;
+  for (int r = q0 + (int)(threadIdx.x & 31); r < q1; r += 32) {
+    int lo, hi;
+    row_interval(g, qs, r, ks, lo, hi);
+    const int a = max(lo, k0), b = min(hi, k1);
+    if (b > a) any = true;
+    if (!(a == k0 && b == k1)) all = false;
+  }
+  any = __any_sync(0xffffffffu, any);
+  all = __all_sync(0xffffffffu, all);
+  return any ? (all ? kKindFull : kKindPartial) : 0;
+}
+
+__global__ void __launch_bounds__(kBuildThreads, 1) build_map_kernel(Geom g, int* __restrict__ ws) {
+  extern __shared__ int sh[];
+  const int NT = g.NT;
+  int* rowlen = sh;              // NT
+  int* collen = sh + NT;         // NT
+  int* scratch = sh + 2 * NT;    // kBuildThreads
+  const int cap = map_capacity(g);
+  MapView mv{ws, NT, cap};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = kBuildThreads / 32;
+  for (int i = tid; i < NT; i += kBuildThreads) collen[i] = 0;
+  // pass 1: row lengths
+  for (int t = warp; t < NT; t += nwarps) {
+    int n = 0;
+    for (int ks = 0; ks < 2; ++ks) {
+      int a, b;
+      candidate_range(g, t, ks, a, b);
+      for (int kt = a; kt < b; ++kt) n += classify_pair_warp(g, t, kt) ? 1 : 0;
+    }
+    if (lane == 0) rowlen[t] = n;
+  }
+  __syncthreads();
+  block_exclusive_scan(rowlen, mv.row_ptr(), NT, scratch);
+  // pass 2: fill row entries, count columns
+  for (int t = warp; t < NT; t += nwarps) {
+    int n = mv.row_ptr()[t];
+    for (int ks = 0; ks < 2; ++ks) {
+      int a, b;
+      candidate_range(g, t, ks, a, b);
+      for (int kt = a; kt < b; ++kt) {
+        const int kind = classify_pair_warp(g, t, kt);
+        if (kind) {
+          if (lane == 0) {
+            mv.row_ent()[n] = entry_make(kt, kind);
+            atomicAdd(&collen[kt], 1);
+          }
+          ++n;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  block_exclusive_scan(collen, mv.col_ptr(), NT, scratch);
+  // pass 3: column entries in increasing q-tile order (binary search in rows)
+  for (int kt = tid; kt < NT; kt += kBuildThreads) {
+    int o = mv.col_ptr()[kt];
+    for (int t = 0; t < NT; ++t) {
+      int lo = mv.row_ptr()[t], hi = mv.row_ptr()[t + 1];
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (entry_tile(mv.row_ent()[mid]) < kt) lo = mid + 1; else hi = mid;
+      }
+      if (lo < mv.row_ptr()[t + 1] && entry_tile(mv.row_ent()[lo]) == kt)
+        mv.col_ent()[o++] = entry_make(t, entry_kind(mv.row_ent()[lo]));
+    }
+  }
+  // pass 4: longest-first orders (stable: ties by index)
+  for (int t = tid; t < NT; t += kBuildThreads) {
+    const int lt = rowlen[t], ct = collen[t];
+    int rr = 0, rc = 0;
+    for (int u = 0; u < NT; ++u) {
+      const int lu = rowlen[u], cu = collen[u];
+      rr += (lu > lt) || (lu == lt && u < t);
+      rc += (cu > ct) || (cu == ct && u < t);
+    }
+    mv.fwd_order()[rr] = t;
+    mv.bwd_order()[rc] = t;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int maxrow = 0;
+    for (int t = 0; t < NT; ++t) maxrow = max(maxrow, rowlen[t]);
+    ws[0] = kMapMagic;
+    ws[1] = g.L;
+    ws[2] = g.xb;
+    ws[3] = g.B;
+    ws[4] = g.NT;
+    ws[5] = g.T0;
+    ws[6] = mv.row_ptr()[NT];
+    ws[7] = maxrow;
+  }
+}
+
+}  // namespace
+
+int build_map_device(const Geom& g, int* ws, cudaStream_t stream) {
+  const size_t smem = (2 * (size_t)g.NT + kBuildThreads) * sizeof(int);
+  if (g.NT > kMaxTiles) return set_error(BD_ERR_UNSUPPORTED, "too many tiles (%d > %d)", g.NT, kMaxTiles);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(build_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    attr_done = true;
+  }
+  build_map_kernel<<<1, kBuildThreads, smem, stream>>>(g, ws);
+  return check_cuda(cudaGetLastError(), "build_map_kernel launch");
+}
+
+}  // namespace bd
+
+// ---------------------------------------------------------------- C ABI
+extern "C" int bd_tilemap_dump(const bd_problem* prob, int32_t* host_out, size_t cap, int64_t* n_tiles) {
+  using namespace bd;
+  int rc = validate_problem(prob);
+  if (rc) return rc;
+  if (!host_out && cap) return set_error(BD_ERR_INVALID_ARG, "host_out is null");
+  const Geom g = geom_of(*prob);
+  std::vector<int> w;
+  build_map_host(g, w);
+  MapView mv{w.data(), g.NT, map_capacity(g)};
+  const int n = mv.row_ptr()[g.NT];
+  if (n_tiles) *n_tiles = n;
+  if (cap < (size_t)n * 5) return set_error(BD_ERR_WORKSPACE, "capacity %zu < %d", cap, n * 5);
+  size_t o = 0;
+  for (int t = 0; t < g.NT; ++t)
+    for (int e = mv.row_ptr()[t]; e < mv.row_ptr()[t + 1]; ++e) {
+      const int kt = entry_tile(mv.row_ent()[e]);
+      host_out[o++] = tile_seg(g, t);
+      host_out[o++] = tile_idx(g, t);
+      host_out[o++] = tile_seg(g, kt);
+      host_out[o++] = tile_idx(g, kt);
+      host_out[o++] = entry_kind(mv.row_ent()[e]);
+    }
+  return BD_OK;
+}
+
+extern "C" int bd_tilemap_stats(const bd_problem* prob, int64_t* out) {
+  using namespace bd;
+  int rc = validate_problem(prob);
+  if (rc) return rc;
+  if (!out) return set_error(BD_ERR_INVALID_ARG, "out is null");
+  const Geom g = geom_of(*prob);
+  std::vector<int> w;
+  build_map_host(g, w);
+  MapView mv{w.data(), g.NT, map_capacity(g)};
+  int64_t full = 0, part = 0;
+  for (int e = 0; e < mv.row_ptr()[g.NT]; ++e) (entry_kind(mv.row_ent()[e]) == kKindFull ? full : part)++;
+  out[0] = g.NT;
+  out[1] = full + part;
+  out[2] = full;
+  out[3] = part;
+  return BD_OK;
+}
+
+// Copies the host-built workspace image of the map (tests compare it with the
+// device-built one).  Not part of the public header's contract beyond tests.
+extern "C" int bd_tilemap_host_image(const bd_problem* prob, int32_t* host_out, size_t cap_words,
+                                     int64_t* n_words) {
+  using namespace bd;
+  int rc = validate_problem(prob);
+  if (rc) return rc;
+  const Geom g = geom_of(*prob);
+  std::vector<int> w;
+  build_map_host(g, w);
+  if (n_words) *n_words = (int64_t)w.size();
+  if (!host_out || cap_words < w.size()) return set_error(BD_ERR_WORKSPACE, "capacity too small");
+  std::copy(w.begin(), w.end(), host_out);
+  return BD_OK;
+}

@@ -1,0 +1,209 @@
+"""Thin Python binding of include/bd_attn.h.
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels of libbdattn.so.  PyTorch supplies device memory, streams and
+process groups.  There is no CPU fallback -- a missing library or a non-CUDA
+tensor raises.
+"""
+
+from dataclasses import dataclass, replace
+import ctypes
+import math
+
+import torch
+
+from . import _lib
+from ._lib import BdProblem, check
+
+TILE = 128
+
+
+@dataclass(frozen=True)
+class Problem:
+    """bd_problem (include/bd_attn.h): prompt/response lengths and block size
+    as in the paper, GQA heads and head_dim."""
+    batch: int
+    prompt_len: int
+    response_len: int
+    block_size: int
+    n_q_heads: int
+    n_kv_heads: int
+    head_dim: int
+    repeat_prompt: int = 1
+    softmax_scale: float = 0.0
+
+    @property
+    def L(self):
+        return self.prompt_len + self.response_len
+
+    @property
+    def xb(self):
+        return 0 if self.repeat_prompt else self.prompt_len
+
+    @property
+    def ntot(self):
+        return 2 * self.L - self.xb
+
+    @property
+    def scale(self):
+        return self.softmax_scale if self.softmax_scale > 0 else 1.0 / math.sqrt(self.head_dim)
+
+    def c(self):
+        return BdProblem(self.batch, self.prompt_len, self.response_len, self.block_size, self.n_q_heads,
+                         self.n_kv_heads, self.head_dim, self.repeat_prompt, float(self.softmax_scale))
+
+    def with_(self, **kw):
+        return replace(self, **kw)
+
+    @staticmethod
+    def from_cfg(cfg, **kw):
+        p = Problem(cfg.batch, cfg.prompt_len, cfg.response_len, cfg.block_size, cfg.n_q_heads,
+                    cfg.n_kv_heads, cfg.head_dim, cfg.repeat_prompt)
+        return p.with_(**kw) if kw else p
+
+
+def _stream_ptr(t):
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise _lib.BdError("bd ops take CUDA tensors only (no CPU fallback)")
+        if not t.is_contiguous():
+            raise _lib.BdError("bd ops take contiguous tensors")
+
+
+_ws_cache = {}
+
+
+def workspace(nbytes, device):
+    """Per-device workspace buffer, grown on demand (caller-owned memory)."""
+    key = torch.device(device).index
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def packed_len(prob: Problem) -> int:
+    p = prob.c()
+    n = _lib.lib().bd_packed_len(ctypes.byref(p))
+    if n < 0:
+        raise _lib.BdError(_lib.lib().bd_last_error().decode())
+    return n
+
+
+def workspace_bytes(prob: Problem, backward: bool) -> int:
+    p = prob.c()
+    return _lib.lib().bd_attn_workspace_bytes(ctypes.byref(p), int(backward))
+
+
+def attn_fwd(prob: Problem, q, k, v, o=None, lse=None):
+    """bd_attn_fwd: returns (o bf16 like q, lse fp32 [b, Hq, Ntot])."""
+    _need_cuda(q, k, v)
+    if o is None:
+        o = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty((prob.batch, prob.n_q_heads, prob.ntot), dtype=torch.float32, device=q.device)
+    p = prob.c()
+    nbytes = _lib.lib().bd_attn_workspace_bytes(ctypes.byref(p), 0)
+    ws = workspace(nbytes, q.device)
+    check(_lib.lib().bd_attn_fwd(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                 lse.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(q)), "bd_attn_fwd")
+    return o, lse
+
+
+def attn_bwd(prob: Problem, q, k, v, o, lse, do, dq=None, dk=None, dv=None):
+    """bd_attn_bwd: returns (dq, dk, dv) bf16."""
+    _need_cuda(q, k, v, o, lse, do)
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    p = prob.c()
+    nbytes = _lib.lib().bd_attn_workspace_bytes(ctypes.byref(p), 1)
+    ws = workspace(nbytes, q.device)
+    check(_lib.lib().bd_attn_bwd(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                 lse.data_ptr(), do.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                                 ws.data_ptr(), ws.numel(), _stream_ptr(q)), "bd_attn_bwd")
+    return dq, dk, dv
+
+
+class BlockDiffusionAttention(torch.autograd.Function):
+    """autograd wrapper: forward = bd_attn_fwd, backward = bd_attn_bwd."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, prob):
+        o, lse = attn_fwd(prob, q, k, v)
+        ctx.save_for_backward(q, k, v, o, lse)
+        ctx.prob = prob
+        return o, lse
+
+    @staticmethod
+    def backward(ctx, do, dlse):
+        q, k, v, o, lse = ctx.saved_tensors
+        dq, dk, dv = attn_bwd(ctx.prob, q, k, v, o, lse, do.contiguous())
+        return dq, dk, dv, None
+
+
+def block_diffusion_attention(q, k, v, prob: Problem):
+    return BlockDiffusionAttention.apply(q, k, v, prob)[0]
+
+
+def logprob(logits, targets, dlogp=None, dlogits=None, lse=None):
+    """bd_logprob over bf16 logits [N, V] (row stride may exceed V).
+
+    Returns logp (and writes dlogits when dlogp is given; dlogits may be
+    `logits` itself for an in-place gradient)."""
+    _need_cuda(targets, dlogp)
+    if not logits.is_cuda or logits.stride(1) != 1:
+        raise _lib.BdError("logits must be a CUDA tensor with unit inner stride")
+    n, V = logits.shape
+    logp = torch.empty(n, dtype=torch.float32, device=logits.device)
+    lse_t = torch.empty(n, dtype=torch.float32, device=logits.device) if lse is None else lse
+    dl_ptr = dlogp.data_ptr() if dlogp is not None else None
+    if dlogp is not None and dlogits is None:
+        dlogits = torch.empty_like(logits)
+    dz_ptr = dlogits.data_ptr() if dlogits is not None else None
+    dz_stride = dlogits.stride(0) if dlogits is not None else 0
+    check(_lib.lib().bd_logprob(n, V, logits.data_ptr(), logits.stride(0), targets.data_ptr(), logp.data_ptr(),
+                                lse_t.data_ptr(), dl_ptr, dz_ptr, dz_stride, _stream_ptr(logits)), "bd_logprob")
+    return (logp, lse_t, dlogits) if dlogp is not None else (logp, lse_t)
+
+
+def tilemap_dump(prob: Problem):
+    """Host path of the tile-map builder: list of (q_seg, q_tile, k_seg, k_tile, kind)."""
+    p = prob.c()
+    n = ctypes.c_int64(0)
+    L = _lib.lib()
+    rc = L.bd_tilemap_dump(ctypes.byref(p), None, 0, ctypes.byref(n))
+    if rc not in (0, 5):
+        check(rc, "bd_tilemap_dump")
+    buf = (ctypes.c_int32 * (5 * n.value))()
+    check(L.bd_tilemap_dump(ctypes.byref(p), buf, 5 * n.value, ctypes.byref(n)), "bd_tilemap_dump")
+    flat = list(buf)
+    return [tuple(flat[i:i + 5]) for i in range(0, len(flat), 5)]
+
+
+def tilemap_stats(prob: Problem):
+    p = prob.c()
+    out = (ctypes.c_int64 * 4)()
+    check(_lib.lib().bd_tilemap_stats(ctypes.byref(p), out), "bd_tilemap_stats")
+    return {"tiles": out[0], "nonempty": out[1], "full": out[2], "partial": out[3]}
+
+
+def tilemap_host_image(prob: Problem):
+    p = prob.c()
+    L = _lib.lib()
+    fn = L.bd_tilemap_host_image
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.POINTER(BdProblem), ctypes.POINTER(ctypes.c_int32), ctypes.c_size_t,
+                   ctypes.POINTER(ctypes.c_int64)]
+    n = ctypes.c_int64(0)
+    fn(ctypes.byref(p), None, 0, ctypes.byref(n))
+    buf = (ctypes.c_int32 * n.value)()
+    check(fn(ctypes.byref(p), buf, n.value, ctypes.byref(n)), "bd_tilemap_host_image")
+    return list(buf)

@@ -1,0 +1,99 @@
+"""CPU tests of the C-ABI library: symbols, validation, host tile-map path
+(bit-exact vs the oracle's dense-mask classification)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2512_22234_b200 as bd
+from paper_2512_22234_b200 import _lib
+from oracle import Problem as OProblem, tilemap
+from workloads import CONFIGS
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "bd_attn.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(bd_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.lib()
+    names = header_functions()
+    assert len(names) >= 10
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+    for n in names:
+        assert n in _lib.SIGNATURES, f"binding lacks {n}"
+
+
+def test_validation_errors():
+    L = _lib.lib()
+    p = bd.Problem(1, 3, 4, 2, 2, 2, 64).c()  # L = 7, B = 2
+    assert L.bd_packed_len(ctypes.byref(p)) == -1
+    assert L.bd_attn_workspace_bytes(ctypes.byref(p), 0) == 0
+    assert b"multiple" in L.bd_last_error()
+    p = bd.Problem(1, 4, 4, 2, 3, 2, 64).c()  # Hq % Hkv != 0
+    assert L.bd_packed_len(ctypes.byref(p)) == -1
+    rc = L.bd_attn_fwd(ctypes.byref(bd.Problem(1, 4, 4, 2, 2, 2, 64).c()), None, None, None, None, None, None, 0,
+                       None)
+    assert rc == 1  # BD_ERR_INVALID_ARG
+    rc = L.bd_attn_fwd(ctypes.byref(bd.Problem(1, 4, 4, 2, 2, 2, 96).c()), 16, 16, 16, 16, 16, 16, 1 << 20, None)
+    assert rc == 3  # BD_ERR_UNSUPPORTED head_dim
+    rc = L.bd_attn_fwd(ctypes.byref(bd.Problem(1, 4, 4, 2, 2, 2, 64).c()), 8, 16, 16, 16, 16, 16, 1 << 20, None)
+    assert rc == 4  # BD_ERR_ALIGNMENT
+    rc = L.bd_attn_fwd(ctypes.byref(bd.Problem(1, 4, 4, 2, 2, 2, 64).c()), 16, 16, 16, 16, 16, 16, 8, None)
+    assert rc == 5  # BD_ERR_WORKSPACE
+    assert L.bd_error_string(5) == b"BD_ERR_WORKSPACE"
+
+
+def test_packed_len_and_workspace():
+    for cfg in CONFIGS.values():
+        p = bd.Problem.from_cfg(cfg)
+        assert bd.packed_len(p) == cfg.ntot
+        assert bd.workspace_bytes(p, True) > bd.workspace_bytes(p, False) > 0
+    p = bd.Problem(1, 10, 20, 5, 1, 1, 64, repeat_prompt=0)
+    assert bd.packed_len(p) == 50
+
+
+def _cases():
+    for P, R, B, rp in [(32, 64, 4, 1), (0, 256, 4, 1), (0, 384, 128, 1), (64, 320, 8, 1), (40, 160, 8, 1),
+                        (40, 160, 8, 0), (100, 300, 4, 0), (0, 512, 256, 1), (0, 512, 1, 1), (24, 0, 1, 0),
+                        (130, 126, 2, 1), (7, 121, 128, 1), (300, 600, 300, 1), (5, 5, 10, 0)]:
+        yield P, R, B, rp
+
+
+@pytest.mark.parametrize("P,R,B,rp", list(_cases()))
+def test_tilemap_bit_exact_vs_oracle(P, R, B, rp):
+    """bd_tilemap_dump == tile kinds read off the oracle's dense mask."""
+    got = bd.tilemap_dump(bd.Problem(1, P, R, B, 1, 1, 64, repeat_prompt=rp))
+    ref = tilemap.classify(OProblem(1, P, R, B, 1, 1, 64, repeat_prompt=rp))
+    assert got == ref
+
+
+@pytest.mark.parametrize("name", ["sdar_1_7b", "sdar_8b", "sweep_b4", "sweep_b32"])
+def test_tilemap_configs_closed_form(name):
+    """Aligned configs: T^2 + 2T non-empty of 4T^2, 3T PARTIAL."""
+    cfg = CONFIGS[name]
+    st = bd.tilemap_stats(bd.Problem.from_cfg(cfg))
+    T = cfg.L // 128
+    assert st["tiles"] == 2 * T
+    assert st["nonempty"] == T * T + 2 * T
+    assert st["partial"] == 3 * T
+
+
+def test_tilemap_sdar_1_7b_vs_oracle_dense():
+    """Bit-exact at a BJ config (L = 2560, dense mask 5120^2)."""
+    cfg = CONFIGS["sdar_1_7b"]
+    got = bd.tilemap_dump(bd.Problem.from_cfg(cfg))
+    ref = tilemap.classify(OProblem(1, cfg.prompt_len, cfg.response_len, cfg.block_size, 1, 1, 128))
+    assert got == ref
+
+
+def test_host_image_layout():
+    img = bd.ops.tilemap_host_image(bd.Problem(1, 32, 64, 4, 2, 2, 64))
+    assert img[0] == 0x42444D31 and img[4] == 2 and img[6] == 3
