@@ -18,8 +18,8 @@ WsLayout ws_layout(const bd_problem& p, int backward) {
   w.map_off = 0;
   size_t off = align256((size_t)map_words(g) * sizeof(int));
   if (backward) {
-    w.dsum_off = off;
-    off = align256(off + (size_t)p.batch * p.n_q_heads * g.N * sizeof(float));
+    w.dsum_off = off;  // tile-major log2-LSE and D vectors
+    off = align256(off + bwd_vec_floats(p, g) * sizeof(float));
     w.dq_off = off;
     off = align256(off + (size_t)p.batch * g.N * p.n_q_heads * p.head_dim * sizeof(float));
   }
@@ -68,4 +68,23 @@ extern "C" int bd_attn_fwd(const bd_problem* prob, const void* q, const void* k,
   int* map = reinterpret_cast<int*>(static_cast<char*>(ws) + wl.map_off);
   if ((rc = build_map_device(g, map, stream))) return rc;
   return run_attn_fwd(*prob, g, q, k, v, o, lse, map, stream);
+}
+
+extern "C" int bd_attn_bwd(const bd_problem* prob, const void* q, const void* k, const void* v, const void* o,
+                           const float* lse, const void* dout, void* dq, void* dk, void* dv, void* ws,
+                           size_t ws_bytes, void* stream_) {
+  using namespace bd;
+  int rc = validate_problem(prob);
+  if (rc) return rc;
+  if ((rc = check_head_dim(*prob))) return rc;
+  if ((rc = check_ptrs({q, k, v, o, lse, dout, dq, dk, dv, ws}))) return rc;
+  const WsLayout wl = ws_layout(*prob, 1);
+  if (ws_bytes < wl.total) return set_error(BD_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, wl.total);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const Geom g = geom_of(*prob);
+  char* w = static_cast<char*>(ws);
+  int* map = reinterpret_cast<int*>(w + wl.map_off);
+  if ((rc = build_map_device(g, map, stream))) return rc;
+  return run_attn_bwd(*prob, g, q, k, v, o, lse, dout, dq, dk, dv, map, reinterpret_cast<float*>(w + wl.dsum_off),
+                      reinterpret_cast<float*>(w + wl.dq_off), stream);
 }

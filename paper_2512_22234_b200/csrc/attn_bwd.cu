@@ -1,0 +1,486 @@
+// bd_attn_bwd: backward of the block-diffusion attention, sm_100a.
+//
+// Analytic gradient of O = softmax(scale QK^T | M) V:
+//   P = exp(scale S - LSE) (masked), dV = P^T dO, dP = dO V^T,
+//   dS = P o (dP - D) with D_i = rowsum(dO_i o O_i),
+//   dQ = scale dS K, dK = scale dS^T Q (dK, dV summed over the q-heads of a group).
+//
+// Kernels:
+//  1. bwd_pre:   D and log2-domain LSE in a tile-major workspace layout (so a
+//                q-tile's 128 values are one aligned 512 B bulk copy), and
+//                zero the fp32 dQ accumulator.
+//  2. bwd_main:  one CTA per (k-tile, sequence, kv head), visiting only the
+//                q-tiles of the tile map's column list (EMPTY tiles never
+//                loaded), for every q-head of the group.  K and V stay in smem;
+//                Q, dO, LSE, D stream through a 2-stage TMA ring.  TMEM holds
+//                S^T [0,128), dP^T [128,256), dV and dK accumulators; P^T (bf16)
+//                overwrites S^T in place and feeds dV += P^T dO from TMEM; dS^T
+//                (bf16) goes to smem and feeds both dK += dS^T Q (K-major A) and
+//                dQ = dS K (MN-major A), the latter into the dP^T columns, from
+//                where the compute warps reduce it into the fp32 dQ accumulator
+//                with vector atomics.
+//  3. bwd_post:  dQ = bf16(scale dQ_acc).
+// Warps 0-7: compute (two warpgroups split the 128 q columns of a tile; a
+// thread owns one key row = one TMEM lane); warp 8: TMA; warp 9: MMA issuer.
+#include "sm100.cuh"
+#include "tma_host.h"
+#include "tilemap.cuh"
+#include "problem.h"
+#include "attn_common.h"
+
+#include <cuda_bf16.h>
+
+namespace bd {
+namespace {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+// ------------------------------------------------------------ preprocess
+// grid: (ceil(N/4), b*Hq); block 128: each warp handles one packed row.
+template <int D>
+__global__ void __launch_bounds__(128) bwd_pre_kernel(const __nv_bfloat16* __restrict__ o,
+                                                      const __nv_bfloat16* __restrict__ dout,
+                                                      const float* __restrict__ lse, float* __restrict__ lse2_t,
+                                                      float* __restrict__ dsum_t, int N, int Hq, Geom g) {
+  const int bh = blockIdx.y;
+  const int b = bh / Hq, h = bh - b * Hq;
+  const int n = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (n >= N) return;
+  const size_t base = (((size_t)b * N + n) * Hq + h) * D;
+  float acc = 0.f;
+  constexpr int kPer = D / 32;  // elements per lane
+  const __nv_bfloat16* po = o + base + lane * kPer;
+  const __nv_bfloat16* pd = dout + base + lane * kPer;
+#pragma unroll
+  for (int i = 0; i < kPer; i += 2) {
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(po + i));
+    const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(pd + i));
+    acc = fmaf(a.x, c.x, fmaf(a.y, c.y, acc));
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) {
+    const int t = n >= g.L ? g.T0 + (n - g.L) / kTileRows : n / kTileRows;
+    const int r = n - tile_start(g, t);
+    const size_t slot = ((size_t)bh * g.NT + t) * kTileRows + r;
+    dsum_t[slot] = acc;
+    lse2_t[slot] = lse[(size_t)bh * N + n] * kLog2e;
+  }
+}
+
+__global__ void zero_kernel(float4* __restrict__ p, size_t n4) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+__global__ void dq_convert_kernel(const float4* __restrict__ acc, uint2* __restrict__ dq, size_t n4, float scale) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 v = acc[i];
+    dq[i] = make_uint2(pack_bf16x2(v.x * scale, v.y * scale), pack_bf16x2(v.z * scale, v.w * scale));
+  }
+}
+
+// ------------------------------------------------------------------ main
+template <int D>
+struct BwdCfg {
+  static constexpr int kTileBytes = 128 * D * 2;
+  static constexpr int kStages = 2;
+  static constexpr int kComputeWarps = 8;
+  static constexpr int kTmaWarp = 8;
+  static constexpr int kMmaWarp = 9;
+  static constexpr int kThreads = 320;
+  static constexpr int kColS = 0, kColDP = 128, kColDV = 256, kColDK = 256 + D;
+  static constexpr uint32_t kTmemCols = 512;
+  // smem: K, V, dS^T, stages x {Q, dO}, stages x {lse2[128], dsum[128]}, barriers
+  static constexpr int kOffK = 0;
+  static constexpr int kOffV = kTileBytes;
+  static constexpr int kOffDS = 2 * kTileBytes;
+  static constexpr int kDsBytes = 128 * 128 * 2;
+  static constexpr int kOffStage = kOffDS + kDsBytes;
+  static constexpr int kStageBytes = 2 * kTileBytes;
+  static constexpr int kOffVec = kOffStage + kStages * kStageBytes;
+  static constexpr int kVecBytes = 2 * 128 * 4;
+  static constexpr int kOffBar = kOffVec + kStages * kVecBytes;
+  // kv_full, qd_full[2], qd_empty[2], s_full, dp_full, compute_done, dv_done, dq_full, dq_empty, acc_done
+  static constexpr int kNumBars = 1 + 2 * kStages + 7;
+  static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16;
+};
+
+struct BwdArgs {
+  const int* map;
+  const float* lse2_t;
+  const float* dsum_t;
+  float* dq_acc;
+  __nv_bfloat16* dk;
+  __nv_bfloat16* dv;
+  int batch, n_q_heads, n_kv_heads, group, N;
+  Geom g;
+  float scale, scale_log2;
+};
+
+template <int D>
+__global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                    const BwdArgs a) {
+  using C = BwdCfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sK = smem + C::kOffK;
+  uint8_t* sV = smem + C::kOffV;
+  uint8_t* sDS = smem + C::kOffDS;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* kv_full = bars;
+  uint64_t* qd_full = bars + 1;
+  uint64_t* qd_empty = qd_full + C::kStages;
+  uint64_t* s_full = qd_empty + C::kStages;
+  uint64_t* dp_full = s_full + 1;
+  uint64_t* compute_done = dp_full + 1;
+  uint64_t* dv_done = compute_done + 1;
+  uint64_t* dq_full = dv_done + 1;
+  uint64_t* dq_empty = dq_full + 1;
+  uint64_t* acc_done = dq_empty + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
+
+  const int warp = (int)warp_id(), lane = (int)lane_id();
+  const Geom& g = a.g;
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
+
+  // ---- work unit: LPT rank of the k-tile, then (sequence, kv head)
+  const int per_tile = a.batch * a.n_kv_heads;
+  const int rank = blockIdx.x / per_tile;
+  const int rem = blockIdx.x - rank * per_tile;
+  const int b = rem / a.n_kv_heads;
+  const int kvh = rem - b * a.n_kv_heads;
+  const MapView mv{const_cast<int*>(a.map), g.NT, map_capacity(g)};
+  const int kt = mv.bwd_order()[rank];
+  const int e0 = mv.col_ptr()[kt];
+  const int n_qt = mv.col_ptr()[kt + 1] - e0;
+  const int* ents = mv.col_ent() + e0;
+  const int n_it = n_qt * a.group;
+  const int k0 = tile_start(g, kt), k1 = tile_end(g, kt), kseg = tile_seg(g, kt);
+
+  if (warp == 0) tmem_alloc<C::kTmemCols>(tslot);
+  if (warp == C::kTmaWarp && lane == 0) {
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&qd_full[s], 1);
+      mbar_init(&qd_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(compute_done, C::kComputeWarps);
+    mbar_init(dv_done, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, C::kComputeWarps);
+    mbar_init(acc_done, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == C::kTmaWarp) {
+    // ================================================================ TMA
+    if (elect_one() && n_it > 0) {
+      mbar_expect_tx(kv_full, 2 * C::kTileBytes);
+      for (int kb = 0; kb < D / 64; ++kb) {
+        tma_load_4d(sK + kb * 16384, &tmK, kv_full, kb * 64, kvh, k0, b);
+        tma_load_4d(sV + kb * 16384, &tmV, kv_full, kb * 64, kvh, k0, b);
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < n_it; ++i) {
+        const int qt = entry_tile(ents[i / a.group]);
+        const int h = kvh * a.group + (i % a.group);
+        const int q0 = tile_start(g, qt);
+        mbar_wait(&qd_empty[stage], phase ^ 1);
+        mbar_expect_tx(&qd_full[stage], 2 * C::kTileBytes + C::kVecBytes);
+        uint8_t* sq = smem + C::kOffStage + stage * C::kStageBytes;
+        for (int kb = 0; kb < D / 64; ++kb) {
+          tma_load_4d(sq + kb * 16384, &tmQ, &qd_full[stage], kb * 64, h, q0, b);
+          tma_load_4d(sq + C::kTileBytes + kb * 16384, &tmO, &qd_full[stage], kb * 64, h, q0, b);
+        }
+        const size_t vec = (((size_t)b * a.n_q_heads + h) * g.NT + qt) * kTileRows;
+        float* sv = reinterpret_cast<float*>(smem + C::kOffVec + stage * C::kVecBytes);
+        bulk_load(sv, a.lse2_t + vec, 512, &qd_full[stage]);
+        bulk_load(sv + 128, a.dsum_t + vec, 512, &qd_full[stage]);
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == C::kMmaWarp) {
+    // ================================================================ MMA
+    if (elect_one() && n_it > 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);  // S^T, dP^T
+      constexpr uint32_t idesc_kv = umma_idesc_bf16(128, D, false, true);    // dV, dK: B MN-major
+      constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, true, true);      // dQ: A, B MN-major
+      const uint32_t kaddr = smem_u32(sK), vaddr = smem_u32(sV), dsaddr = smem_u32(sDS);
+      auto issue_s = [&](int stage) {
+        const uint32_t qaddr = smem_u32(smem + C::kOffStage + stage * C::kStageBytes);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+          umma_ss(tbase + C::kColS, umma_desc_sw128(kaddr + off, 16, 1024), umma_desc_sw128(qaddr + off, 16, 1024),
+                  idesc_s, k > 0);
+        }
+        umma_commit(s_full);
+      };
+      auto issue_dp = [&](int stage) {
+        const uint32_t doaddr = smem_u32(smem + C::kOffStage + stage * C::kStageBytes + C::kTileBytes);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+          umma_ss(tbase + C::kColDP, umma_desc_sw128(vaddr + off, 16, 1024),
+                  umma_desc_sw128(doaddr + off, 16, 1024), idesc_s, k > 0);
+        }
+        umma_commit(dp_full);
+      };
+      mbar_wait(kv_full, 0);
+      mbar_wait(&qd_full[0], 0);
+      tc_fence_after();
+      issue_s(0);
+      issue_dp(0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < n_it; ++i) {
+        const uint32_t qaddr = smem_u32(smem + C::kOffStage + stage * C::kStageBytes);
+        const uint32_t doaddr = qaddr + C::kTileBytes;
+        mbar_wait(compute_done, i & 1);
+        tc_fence_after();
+        // dV += P^T dO   (A = P^T in TMEM: q 0..63 at cols [0,32), q 64..127 at [64,96))
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          umma_ts(tbase + C::kColDV, tbase + C::kColS + (k < 4 ? k * 8 : 64 + (k - 4) * 8),
+                  umma_desc_sw128(doaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
+        umma_commit(dv_done);
+        // dK += dS^T Q   (A = dS^T smem K-major, B = Q MN-major)
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          umma_ss(tbase + C::kColDK, umma_desc_sw128(dsaddr + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024),
+                  umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
+        // dQ = dS K      (A = dS^T smem read MN-major, B = K MN-major) -> dP^T columns
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          umma_ss(tbase + C::kColDP, umma_desc_sw128(dsaddr + k * 2048, 16384, 1024),
+                  umma_desc_sw128(kaddr + k * 2048, 16384, 1024), idesc_q, k > 0);
+        umma_commit(dq_full);
+        umma_commit(&qd_empty[stage]);
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (i + 1 < n_it) {
+          mbar_wait(dv_done, i & 1);  // P^T(i) consumed -> S^T columns free
+          mbar_wait(&qd_full[stage], phase);
+          tc_fence_after();
+          issue_s(stage);
+          mbar_wait(dq_empty, i & 1);  // dQ(i) drained -> dP^T columns free
+          tc_fence_after();
+          issue_dp(stage);
+        }
+      }
+      umma_commit(acc_done);
+    }
+  } else {
+    // ========================================================== compute
+    const int wg = warp >> 2;                 // q-column half
+    const int r = (warp & 3) * 32 + lane;     // key row within the tile == TMEM lane
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const float sl2 = a.scale_log2;
+    const int kpos = k0 + r;                  // packed key column of this thread
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i = 0; i < n_it; ++i) {
+      const int ent = ents[i / a.group];
+      const int qt = entry_tile(ent);
+      const int h = kvh * a.group + (i % a.group);
+      const int q0 = tile_start(g, qt), q1 = tile_end(g, qt), qseg = tile_seg(g, qt);
+      const bool need_mask = entry_kind(ent) == kKindPartial || (q1 - q0) < 128 || (k1 - k0) < 128;
+      const float* sv = reinterpret_cast<const float*>(smem + C::kOffVec + stage * C::kVecBytes);
+      mbar_wait(&qd_full[stage], phase);  // LSE / D of this q-tile landed
+      mbar_wait(s_full, i & 1);
+      mbar_wait(dp_full, i & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int cb = wg * 64 + c * 32;  // first q column of this chunk
+        uint32_t sr[32], dr[32];
+        tmem_ld32(tbase + lane_off + C::kColS + cb, sr);
+        tmem_ld32(tbase + lane_off + C::kColDP + cb, dr);
+        tmem_ld_wait();
+        float pv[32], ds[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float p = ex2_approx(fmaf(__uint_as_float(sr[j]), sl2, -sv[cb + j]));
+          pv[j] = p;
+          ds[j] = p * (__uint_as_float(dr[j]) - sv[128 + cb + j]);
+        }
+        if (need_mask) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int qrow = q0 + cb + j;
+            int lo, hi;
+            row_interval(g, qseg, qrow, kseg, lo, hi);
+            const bool vis = qrow < q1 && kpos < k1 && kpos >= lo && kpos < hi;
+            pv[j] = vis ? pv[j] : 0.f;
+            ds[j] = vis ? ds[j] : 0.f;
+          }
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(pv[2 * j], pv[2 * j + 1]);
+        // P^T (bf16) into this warpgroup's own S^T columns (already read)
+        tmem_st16(tbase + lane_off + C::kColS + wg * 64 + c * 16, pk);
+        // dS^T (bf16) into smem, K-major rows = keys, block wg = q half
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(ds[2 * j], ds[2 * j + 1]);
+        uint8_t* dsrow = sDS + wg * 16384;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          *reinterpret_cast<uint4*>(dsrow + sw128_offset(r, c * 4 + u)) =
+              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+      }
+      tmem_st_wait();
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(compute_done);
+      // ---- dQ(i): TMEM (lane = q row) -> fp32 atomics
+      mbar_wait(dq_full, i & 1);
+      tc_fence_after();
+      {
+        const int qrow = q0 + r;
+        float* dst = a.dq_acc + (((size_t)b * a.N + qrow) * a.n_q_heads + h) * D + wg * (D / 2);
+        const bool ok = qrow < q1;
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tbase + lane_off + C::kColDP + wg * (D / 2) + 32 * c, v);
+          tmem_ld_wait();
+          if (ok) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              red_add_v4(dst + 32 * c + 4 * u, __uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1]),
+                         __uint_as_float(v[4 * u + 2]), __uint_as_float(v[4 * u + 3]));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_empty);
+      if (++stage == C::kStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    // ---- epilogue: dK (scaled), dV -> bf16
+    if (n_it > 0) {
+      mbar_wait(acc_done, 0);
+      tc_fence_after();
+    }
+    const bool ok = kpos < k1;
+    const size_t orow = (((size_t)b * a.N + kpos) * a.n_kv_heads + kvh) * D + wg * (D / 2);
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t col = (which ? C::kColDK : C::kColDV) + wg * (D / 2);
+      const float mul = which ? a.scale : 1.f;
+      __nv_bfloat16* out = (which ? a.dk : a.dv) + orow;
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tbase + lane_off + col + 32 * c, v);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          pk[j] = n_it > 0 ? pack_bf16x2(__uint_as_float(v[2 * j]) * mul, __uint_as_float(v[2 * j + 1]) * mul) : 0u;
+        if (ok) {
+          uint4* dst = reinterpret_cast<uint4*>(out + 32 * c);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dst[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<C::kTmemCols>(tbase);
+}
+
+template <int D>
+int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, const void* o,
+               const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, float* vec_ws,
+               float* dq_acc, cudaStream_t stream) {
+  using C = BwdCfg<D>;
+  const int Hq = p.n_q_heads;
+  const size_t nvec = (size_t)p.batch * Hq * g.NT * kTileRows;
+  float* lse2_t = vec_ws;
+  float* dsum_t = vec_ws + nvec;
+  const size_t nacc = (size_t)p.batch * g.N * Hq * D;
+  // 1. zero the dQ accumulator and the padded vectors; D and log2 LSE
+  zero_kernel<<<1184, 256, 0, stream>>>(reinterpret_cast<float4*>(dq_acc), nacc / 4);
+  zero_kernel<<<296, 256, 0, stream>>>(reinterpret_cast<float4*>(vec_ws), 2 * nvec / 4);
+  {
+    dim3 grid((g.N + 3) / 4, p.batch * Hq);
+    bwd_pre_kernel<D><<<grid, 128, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
+                                                 reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2_t, dsum_t,
+                                                 g.N, Hq, g);
+  }
+  // 2. main
+  CUtensorMap tmQ, tmK, tmV, tmO;
+  if (!make_qkv_tmap(&tmQ, q, p.batch, g.N, Hq, D) || !make_qkv_tmap(&tmK, k, p.batch, g.N, p.n_kv_heads, D) ||
+      !make_qkv_tmap(&tmV, v, p.batch, g.N, p.n_kv_heads, D) || !make_qkv_tmap(&tmO, dout, p.batch, g.N, Hq, D))
+    return set_error(BD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e =
+        cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(bwd)");
+    attr = true;
+  }
+  BwdArgs a;
+  a.map = map;
+  a.lse2_t = lse2_t;
+  a.dsum_t = dsum_t;
+  a.dq_acc = dq_acc;
+  a.dk = reinterpret_cast<__nv_bfloat16*>(dk);
+  a.dv = reinterpret_cast<__nv_bfloat16*>(dv);
+  a.batch = p.batch;
+  a.n_q_heads = Hq;
+  a.n_kv_heads = p.n_kv_heads;
+  a.group = Hq / p.n_kv_heads;
+  a.N = g.N;
+  a.g = g;
+  a.scale = scale_of(p);
+  a.scale_log2 = a.scale * kLog2e;
+  const long long grid = (long long)g.NT * p.batch * p.n_kv_heads;
+  attn_bwd_kernel<D><<<(unsigned)grid, C::kThreads, C::kSmemBytes, stream>>>(tmQ, tmK, tmV, tmO, a);
+  int rc = check_cuda(cudaGetLastError(), "attn_bwd_kernel launch");
+  if (rc) return rc;
+  // 3. dQ = bf16(scale * acc)
+  dq_convert_kernel<<<1184, 256, 0, stream>>>(reinterpret_cast<const float4*>(dq_acc), reinterpret_cast<uint2*>(dq),
+                                              nacc / 4, a.scale);
+  return check_cuda(cudaGetLastError(), "dq_convert launch");
+}
+
+}  // namespace
+
+size_t bwd_vec_floats(const bd_problem& p, const Geom& g) {
+  return 2 * (size_t)p.batch * p.n_q_heads * g.NT * kTileRows;
+}
+
+int run_attn_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, const void* o,
+                 const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, float* vec_ws,
+                 float* dq_acc, cudaStream_t stream) {
+  if (p.head_dim == 128)
+    return launch_bwd<128>(p, g, q, k, v, o, lse, dout, dq, dk, dv, map, vec_ws, dq_acc, stream);
+  if (p.head_dim == 64)
+    return launch_bwd<64>(p, g, q, k, v, o, lse, dout, dq, dk, dv, map, vec_ws, dq_acc, stream);
+  return set_error(BD_ERR_UNSUPPORTED, "head_dim %d not in {64, 128}", p.head_dim);
+}
+
+}  // namespace bd

@@ -21,7 +21,8 @@ int build_map_device(const Geom& g, int* ws, cudaStream_t stream);
 int run_attn_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, void* o,
                  float* lse, const int* map, cudaStream_t stream);
 int run_attn_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, const void* o,
-                 const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, float* dsum,
+                 const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, float* vec_ws,
                  float* dq_acc, cudaStream_t stream);
+size_t bwd_vec_floats(const bd_problem& p, const Geom& g);
 
 }  // namespace bd
