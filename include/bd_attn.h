@@ -118,6 +118,14 @@ int bd_attn_bwd(const bd_problem* prob, const void* q, const void* k, const void
 int bd_logprob(int64_t n_rows, int32_t vocab, const void* logits, int64_t row_stride, const int32_t* targets,
                float* logp, float* lse, const float* dlogp, void* dlogits, int64_t dlogits_stride, void* stream);
 
+/* Gradient of bd_logprob from a known LSE (one read of the logits, one
+ * write of the gradient), for when dlogp depends on logp (clipped ratios):
+ *   dlogits[n, v] = dlogp_n (1[v = t_n] - exp(z[n, v] - lse_n)).
+ * Arguments as in bd_logprob; lse is the fp32 [n_rows] output of bd_logprob;
+ * dlogits may alias logits (in place, equal strides). */
+int bd_logprob_bwd(int64_t n_rows, int32_t vocab, const void* logits, int64_t row_stride, const int32_t* targets,
+                   const float* lse, const float* dlogp, void* dlogits, int64_t dlogits_stride, void* stream);
+
 /* DiPO, step 1: per-group partial statistics of the local trajectories.
  *   rewards        fp32 [n_traj]       r_i
  *   group_of_traj  int32 [n_traj]      global group id in [0, n_groups)
@@ -156,6 +164,10 @@ int bd_tilemap_stats(const bd_problem* prob, int64_t* out);
 
 const char* bd_error_string(int code);
 const char* bd_last_error(void);
+
+/* Number of CUDA kernels this library has enqueued since it was loaded
+ * (process-wide counter; bench.py reports launches per timed region). */
+int64_t bd_launch_count(void);
 
 /* Hardware self-test of the UMMA / TMEM / TMA conventions (diagnostic).
  * a, b, v bf16 [128][128]; c = a.b^T, o_* = bf16(c).v via TMEM-A, smem-A

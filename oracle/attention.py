@@ -129,6 +129,37 @@ def backward_slice(prob: Problem, q, k, v, do, b: int, g: int):
     return dq, dk, dv, o, lse
 
 
+def backward_rows(prob: Problem, q, k, v, do, b: int, h: int, rows):
+    """The same dense backward restricted to query rows ``rows`` of (b, h):
+    returns (dq[rows] [n, d], dk_part [Ntot, d], dv_part [Ntot, d]) where the
+    parts are those rows' contributions to dK / dV.  Used for bounded CPU
+    baselines and sampled parity at full size."""
+    q, k, v, do = _f64(q), _f64(k), _f64(v), _f64(do)
+    g = prob.kv_head_of(h)
+    rows = np.asarray(rows, dtype=np.int64)
+    kg, vg = k[b, :, g, :], v[b, :, g, :]
+    N, d = prob.ntot, prob.head_dim
+    dq = np.zeros((len(rows), d))
+    dk = np.zeros((N, d))
+    dv = np.zeros((N, d))
+    for r0, r1 in _chunks(len(rows), N):
+        rr = rows[r0:r1]
+        m = mask_rows(prob, rr)
+        assert_rows_nonempty(m)
+        s = prob.scale * (q[b, rr, h, :] @ kg.T)
+        s = np.where(m, s, -np.inf)
+        mx = s.max(axis=1, keepdims=True)
+        e = np.exp(s - mx)
+        p = e / e.sum(axis=1, keepdims=True)
+        dO = do[b, rr, h, :]
+        dp = dO @ vg.T
+        ds = p * (dp - (p * dp).sum(axis=1, keepdims=True))
+        dq[r0:r1] = prob.scale * (ds @ kg)
+        dk += prob.scale * (ds.T @ q[b, rr, h, :])
+        dv += p.T @ dO
+    return dq, dk, dv
+
+
 def backward(prob: Problem, q, k, v, do):
     """Full backward: dq like q, dk/dv like k (fp64)."""
     prob.validate()

@@ -41,7 +41,9 @@ SIGNATURES = {
     "bd_attn_fwd": (ctypes.c_int, [_PROB, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "bd_attn_bwd": (ctypes.c_int, [_PROB, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "bd_logprob": (ctypes.c_int, [_I64, _I32, _P, _I64, _P, _P, _P, _P, _P, _I64, _P]),
-    "bd_dipo_group_stats": (ctypes.c_int, [_I32, _P, _P, _P, _I32, _P, _P]),
+    "bd_logprob_bwd": (ctypes.c_int, [_I64, _I32, _P, _I64, _P, _P, _P, _P, _I64, _P]),
+    "bd_launch_count": (_I64, []),
+    "bd_dipo_group_stats":(ctypes.c_int, [_I32, _P, _P, _P, _I32, _P, _P]),
     "bd_dipo_token_loss": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P, _I32, _F, _P, _P, _P]),
     "bd_tilemap_dump": (ctypes.c_int, [_PROB, ctypes.POINTER(_I32), _SZ, ctypes.POINTER(_I64)]),
     "bd_tilemap_stats": (ctypes.c_int, [_PROB, ctypes.POINTER(_I64)]),

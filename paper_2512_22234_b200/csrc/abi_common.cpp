@@ -3,10 +3,14 @@
 
 #include <cstdio>
 #include <cstdarg>
+#include <atomic>
 
 namespace bd {
 
 static thread_local char g_last_error[512] = "";
+static std::atomic<long long> g_launches{0};
+
+void note_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 int set_error(int code, const char* fmt, ...) {
   va_list ap;
@@ -37,3 +41,5 @@ extern "C" const char* bd_error_string(int code) {
 }
 
 extern "C" const char* bd_last_error(void) { return bd::g_last_error; }
+
+extern "C" int64_t bd_launch_count(void) { return bd::g_launches.load(std::memory_order_relaxed); }

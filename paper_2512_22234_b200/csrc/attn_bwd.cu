@@ -459,6 +459,7 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   a.scale_log2 = a.scale * kLog2e;
   const long long grid = (long long)g.NT * p.batch * p.n_kv_heads;
   attn_bwd_kernel<D><<<(unsigned)grid, C::kThreads, C::kSmemBytes, stream>>>(tmQ, tmK, tmV, tmO, a);
+  note_launches(5);  // zero x2, pre, main, convert (below)
   int rc = check_cuda(cudaGetLastError(), "attn_bwd_kernel launch");
   if (rc) return rc;
   // 3. dQ = bf16(scale * acc)

@@ -330,6 +330,7 @@ int launch_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   const long long grid = (long long)g.NT * p.batch * a.n_hg;
   if (grid > 0x7FFFFFFF) return set_error(BD_ERR_UNSUPPORTED, "grid too large");
   attn_fwd_kernel<D, NQ><<<(unsigned)grid, C::kThreads, C::kSmemBytes, stream>>>(tmQ, tmK, tmV, a);
+  note_launches(1);
   return check_cuda(cudaGetLastError(), "attn_fwd_kernel launch");
 }
 

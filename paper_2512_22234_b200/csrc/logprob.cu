@@ -1,0 +1,220 @@
+// bd_logprob: per-token log-softmax gather over the vocabulary, optionally
+// fused with its gradient (P:150-156 numerators of Eqs. 6-8; P:78 CE of Eq. 3;
+// S:69-77).  HBM-streaming: one CTA per row.
+//   pass 1: online (max, sum-exp) over the row in fp32 -> LSE_n; logp_n = z[t] - LSE_n
+//   pass 2 (dlogp given): dz[v] = w_n (1[v = t_n] - exp(z[v] - LSE_n)), re-reading
+//           the row (L2-resident: it was just streamed by pass 1).
+// Rows are read with 16-byte vector loads when the row is 16-byte aligned and
+// V % 8 == 0 (Qwen3 V = 151,936 is), otherwise element-wise.
+#include "abi_common.h"
+#include "sm100.cuh"
+
+#include <cuda_bf16.h>
+
+namespace bd {
+namespace {
+
+constexpr int kThreads = 512;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.69314718055994531f;
+
+__device__ __forceinline__ void online_add(float& m, float& s, float x) {
+  // running max m (log2 units) and sum s of 2^(x - m)
+  if (x > m) {
+    s = s * ex2_approx(m - x) + 1.f;
+    m = x;
+  } else {
+    s += ex2_approx(x - m);
+  }
+}
+
+__device__ __forceinline__ void online_merge(float& m, float& s, float m2, float s2) {
+  const float mm = fmaxf(m, m2);
+  if (mm == -INFINITY) return;
+  s = s * ex2_approx(m - mm) + s2 * ex2_approx(m2 - mm);
+  m = mm;
+}
+
+__device__ __forceinline__ ulonglong2 ld_stream(const void* p) {
+  ulonglong2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p));
+  return r;
+}
+
+__global__ void __launch_bounds__(kThreads) logprob_kernel(int64_t n_rows, int V, const __nv_bfloat16* __restrict__ z,
+                                                           int64_t stride, const int32_t* __restrict__ targets,
+                                                           float* __restrict__ logp, float* __restrict__ lse_out,
+                                                           const float* __restrict__ dlogp,
+                                                           __nv_bfloat16* dz, int64_t dz_stride) {
+  __shared__ float sm_m[kThreads / 32], sm_s[kThreads / 32];
+  __shared__ float s_lse;
+  const int64_t row = blockIdx.x;
+  if (row >= n_rows) return;
+  const __nv_bfloat16* zr = z + row * stride;
+  const int tid = threadIdx.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(zr) & 15) == 0) && (V % 8 == 0);
+  float m = -INFINITY, s = 0.f;
+  if (vec) {
+    const int nv = V / 8;
+    for (int i = tid; i < nv; i += kThreads) {
+      const ulonglong2 u = ld_stream(zr + 8 * i);
+      const uint32_t w[4] = {(uint32_t)u.x, (uint32_t)(u.x >> 32), (uint32_t)u.y, (uint32_t)(u.y >> 32)};
+      float x[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        x[2 * j] = __uint_as_float(w[j] << 16) * kLog2e;
+        x[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u) * kLog2e;
+      }
+      float mx = x[0];
+#pragma unroll
+      for (int j = 1; j < 8; ++j) mx = fmaxf(mx, x[j]);
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc += ex2_approx(x[j] - mx);
+      online_merge(m, s, mx, acc);
+    }
+  } else {
+    for (int i = tid; i < V; i += kThreads) online_add(m, s, __bfloat162float(zr[i]) * kLog2e);
+  }
+  // block reduce (m, s)
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, off);
+    online_merge(m, s, m2, s2);
+  }
+  if ((tid & 31) == 0) {
+    sm_m[tid >> 5] = m;
+    sm_s[tid >> 5] = s;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    m = tid < kThreads / 32 ? sm_m[tid] : -INFINITY;
+    s = tid < kThreads / 32 ? sm_s[tid] : 0.f;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+      const float s2 = __shfl_xor_sync(0xffffffffu, s, off);
+      online_merge(m, s, m2, s2);
+    }
+    if (tid == 0) {
+      const float lse = (m + __log2f(s)) * kLn2;
+      s_lse = lse;
+      const int t = targets[row];
+      const bool ok = t >= 0 && t < V;
+      logp[row] = ok ? __bfloat162float(zr[t]) - lse : __int_as_float(0x7fc00000);
+      if (lse_out) lse_out[row] = lse;
+    }
+  }
+  if (!dlogp || !dz) return;
+  __syncthreads();
+  const float lse2 = s_lse * kLog2e;
+  const float w = dlogp[row];
+  const int t = targets[row];
+  __nv_bfloat16* dr = dz + row * dz_stride;
+  const bool vec2 = vec && ((reinterpret_cast<uintptr_t>(dr) & 15) == 0);
+  if (vec2) {
+    const int nv = V / 8;
+    for (int i = tid; i < nv; i += kThreads) {
+      const uint4 u = *reinterpret_cast<const uint4*>(zr + 8 * i);
+      const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int v0 = 8 * i + 2 * j;
+        float p0 = ex2_approx(fmaf(__uint_as_float(wd[j] << 16), kLog2e, -lse2));
+        float p1 = ex2_approx(fmaf(__uint_as_float(wd[j] & 0xFFFF0000u), kLog2e, -lse2));
+        const float g0 = w * ((v0 == t ? 1.f : 0.f) - p0);
+        const float g1 = w * ((v0 + 1 == t ? 1.f : 0.f) - p1);
+        o[j] = pack_bf16x2(g0, g1);
+      }
+      *reinterpret_cast<uint4*>(dr + 8 * i) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  } else {
+    for (int i = tid; i < V; i += kThreads) {
+      const float p = ex2_approx(fmaf(__bfloat162float(zr[i]), kLog2e, -lse2));
+      dr[i] = __float2bfloat16(w * ((i == t ? 1.f : 0.f) - p));
+    }
+  }
+}
+
+// dz = w (1[v = t] - exp(z - LSE)) from a known LSE: one read + one write.
+__global__ void __launch_bounds__(kThreads) logprob_bwd_kernel(int64_t n_rows, int V,
+                                                               const __nv_bfloat16* z, int64_t stride,
+                                                               const int32_t* __restrict__ targets,
+                                                               const float* __restrict__ lse,
+                                                               const float* __restrict__ dlogp, __nv_bfloat16* dz,
+                                                               int64_t dz_stride) {
+  const int64_t row = blockIdx.x;
+  if (row >= n_rows) return;
+  const __nv_bfloat16* zr = z + row * stride;
+  __nv_bfloat16* dr = dz + row * dz_stride;
+  const float lse2 = lse[row] * kLog2e;
+  const float w = dlogp[row];
+  const int t = targets[row];
+  const int tid = threadIdx.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(zr) & 15) == 0) && ((reinterpret_cast<uintptr_t>(dr) & 15) == 0) &&
+                   (V % 8 == 0);
+  if (vec) {
+    const int nv = V / 8;
+    for (int i = tid; i < nv; i += kThreads) {
+      const uint4 u = *reinterpret_cast<const uint4*>(zr + 8 * i);
+      const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int v0 = 8 * i + 2 * j;
+        const float p0 = ex2_approx(fmaf(__uint_as_float(wd[j] << 16), kLog2e, -lse2));
+        const float p1 = ex2_approx(fmaf(__uint_as_float(wd[j] & 0xFFFF0000u), kLog2e, -lse2));
+        o[j] = pack_bf16x2(w * ((v0 == t ? 1.f : 0.f) - p0), w * ((v0 + 1 == t ? 1.f : 0.f) - p1));
+      }
+      *reinterpret_cast<uint4*>(dr + 8 * i) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  } else {
+    for (int i = tid; i < V; i += kThreads) {
+      const float p = ex2_approx(fmaf(__bfloat162float(zr[i]), kLog2e, -lse2));
+      dr[i] = __float2bfloat16(w * ((i == t ? 1.f : 0.f) - p));
+    }
+  }
+}
+
+}  // namespace
+}  // namespace bd
+
+extern "C" int bd_logprob_bwd(int64_t n_rows, int32_t vocab, const void* logits, int64_t row_stride,
+                              const int32_t* targets, const float* lse, const float* dlogp, void* dlogits,
+                              int64_t dlogits_stride, void* stream_) {
+  using namespace bd;
+  if (n_rows < 0 || vocab <= 0 || row_stride < vocab || dlogits_stride < vocab)
+    return set_error(BD_ERR_INVALID_ARG, "bad logprob shape");
+  if (n_rows == 0) return BD_OK;
+  if (!logits || !targets || !lse || !dlogp || !dlogits) return set_error(BD_ERR_INVALID_ARG, "null pointer");
+  if (dlogits == logits && dlogits_stride != row_stride)
+    return set_error(BD_ERR_INVALID_ARG, "in-place gradient needs equal strides");
+  if (n_rows > 0x7FFFFFFF) return set_error(BD_ERR_UNSUPPORTED, "too many rows");
+  logprob_bwd_kernel<<<(unsigned)n_rows, kThreads, 0, static_cast<cudaStream_t>(stream_)>>>(
+      n_rows, vocab, reinterpret_cast<const __nv_bfloat16*>(logits), row_stride, targets, lse, dlogp,
+      reinterpret_cast<__nv_bfloat16*>(dlogits), dlogits_stride);
+  note_launches(1);
+  return check_cuda(cudaGetLastError(), "logprob_bwd_kernel launch");
+}
+
+extern "C" int bd_logprob(int64_t n_rows, int32_t vocab, const void* logits, int64_t row_stride,
+                          const int32_t* targets, float* logp, float* lse, const float* dlogp, void* dlogits,
+                          int64_t dlogits_stride, void* stream_) {
+  using namespace bd;
+  if (n_rows < 0 || vocab <= 0 || row_stride < vocab) return set_error(BD_ERR_INVALID_ARG, "bad logprob shape");
+  if (n_rows == 0) return BD_OK;
+  if (!logits || !targets || !logp) return set_error(BD_ERR_INVALID_ARG, "null pointer");
+  if (dlogp && !dlogits) return set_error(BD_ERR_INVALID_ARG, "dlogp given without dlogits");
+  if (dlogits && dlogits_stride < vocab) return set_error(BD_ERR_INVALID_ARG, "bad dlogits stride");
+  if (dlogits == logits && dlogits_stride != row_stride)
+    return set_error(BD_ERR_INVALID_ARG, "in-place gradient needs equal strides");
+  if (n_rows > 0x7FFFFFFF) return set_error(BD_ERR_UNSUPPORTED, "too many rows");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  logprob_kernel<<<(unsigned)n_rows, kThreads, 0, stream>>>(
+      n_rows, vocab, reinterpret_cast<const __nv_bfloat16*>(logits), row_stride, targets, logp, lse, dlogp,
+      reinterpret_cast<__nv_bfloat16*>(dlogits), dlogits_stride);
+  note_launches(1);
+  return check_cuda(cudaGetLastError(), "logprob_kernel launch");
+}

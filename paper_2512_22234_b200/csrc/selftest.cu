@@ -7,7 +7,7 @@
 // A, B, V are [128][128] bf16 row-major.  Exported as bd_selftest_mma.
 #include "sm100.cuh"
 #include "tma_host.h"
-#include "bd_attn.h"
+#include "abi_common.h"
 
 #include <cuda_bf16.h>
 
@@ -161,5 +161,6 @@ extern "C" int bd_selftest_mma(const void* a, const void* b, const void* v, floa
     return BD_ERR_CUDA;
   selftest_kernel<<<1, 128, smem, stream>>>(reinterpret_cast<const __nv_bfloat16*>(a), tmB, tmV, c, o_ts, o_ss,
                                             o_mn);
+  note_launches(1);
   return cudaGetLastError() == cudaSuccess ? BD_OK : BD_ERR_CUDA;
 }

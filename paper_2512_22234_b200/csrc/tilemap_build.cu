@@ -203,6 +203,7 @@ int build_map_device(const Geom& g, int* ws, cudaStream_t stream) {
     attr_done = true;
   }
   build_map_kernel<<<1, kBuildThreads, smem, stream>>>(g, ws);
+  note_launches(1);
   return check_cuda(cudaGetLastError(), "build_map_kernel launch");
 }
 

@@ -207,3 +207,47 @@ def tilemap_host_image(prob: Problem):
     buf = (ctypes.c_int32 * n.value)()
     check(fn(ctypes.byref(p), buf, n.value, ctypes.byref(n)), "bd_tilemap_host_image")
     return list(buf)
+
+
+def logprob_bwd(logits, targets, lse, dlogp, dlogits=None):
+    """bd_logprob_bwd: dlogits = dlogp (onehot - softmax) from a known LSE (may be in place)."""
+    _need_cuda(targets, lse, dlogp)
+    if not logits.is_cuda or logits.stride(1) != 1:
+        raise _lib.BdError("logits must be a CUDA tensor with unit inner stride")
+    n, V = logits.shape
+    if dlogits is None:
+        dlogits = torch.empty_like(logits)
+    check(_lib.lib().bd_logprob_bwd(n, V, logits.data_ptr(), logits.stride(0), targets.data_ptr(), lse.data_ptr(),
+                                    dlogp.data_ptr(), dlogits.data_ptr(), dlogits.stride(0), _stream_ptr(logits)),
+          "bd_logprob_bwd")
+    return dlogits
+
+
+def launch_count() -> int:
+    """Kernels enqueued by libbdattn.so so far (process-wide)."""
+    return int(_lib.lib().bd_launch_count())
+
+
+def dipo_group_stats(rewards, group_of_traj, traj_len, n_groups, out=None):
+    """bd_dipo_group_stats: fp64 [n_groups, 3] += (sum r, count, sum |tau|)."""
+    _need_cuda(rewards, group_of_traj, traj_len)
+    if out is None:
+        out = torch.zeros((n_groups, 3), dtype=torch.float64, device=rewards.device)
+    check(_lib.lib().bd_dipo_group_stats(rewards.numel(), rewards.data_ptr(), group_of_traj.data_ptr(),
+                                         traj_len.data_ptr(), n_groups, out.data_ptr(), _stream_ptr(rewards)),
+          "bd_dipo_group_stats")
+    return out
+
+
+def dipo_token_loss(logp, logp_old, traj_of_token, rewards, group_of_traj, group_stats, n_groups_global,
+                    eps=0.2, partials=None):
+    """bd_dipo_token_loss: returns (dlogp fp32 [n], partials fp64 [3] += (loss, tokens, clipped))."""
+    _need_cuda(logp, logp_old, traj_of_token, rewards, group_of_traj, group_stats)
+    dlogp = torch.empty_like(logp)
+    if partials is None:
+        partials = torch.zeros(3, dtype=torch.float64, device=logp.device)
+    check(_lib.lib().bd_dipo_token_loss(logp.numel(), logp.data_ptr(), logp_old.data_ptr(), traj_of_token.data_ptr(),
+                                        rewards.data_ptr(), group_of_traj.data_ptr(), group_stats.data_ptr(),
+                                        int(n_groups_global), float(eps), dlogp.data_ptr(), partials.data_ptr(),
+                                        _stream_ptr(logp)), "bd_dipo_token_loss")
+    return dlogp, partials

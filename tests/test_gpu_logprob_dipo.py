@@ -1,0 +1,91 @@
+"""GPU parity of bd_logprob / bd_logprob_bwd / DiPO kernels vs the fp64 oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2512_22234_b200 as bd
+from paper_2512_22234_b200 import ops, dipo as bdipo
+from oracle import logprob as olp, dipo as odipo
+from parity import LOGP_MAX_ABS, DZ_REL_L2, metrics, t2np
+from workloads import logits_inputs, rl_batch, VOCAB_QWEN3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,V,peaked", [(64, 1024, False), (64, VOCAB_QWEN3, False), (33, VOCAB_QWEN3, True),
+                                        (17, 1001, False), (1, 8, False)])
+def test_logprob_fwd_bwd(cuda_ok, n, V, peaked):
+    z, t = logits_inputs(n, V, seed=n + V, peaked=peaked)
+    w = torch.randn(n, generator=torch.Generator().manual_seed(5), dtype=torch.float32)
+    zc, tc, wc = z.cuda(), t.cuda(), w.cuda()
+    logp, lse = ops.logprob(zc, tc)
+    logp2, lse2, dz = ops.logprob(zc, tc, dlogp=wc)
+    dz2 = ops.logprob_bwd(zc, tc, lse, wc)
+    torch.cuda.synchronize()
+    ref_lp, ref_lse = olp.logprob(z, t.long())
+    ref_dz = olp.logprob_grad(z, t.long(), w.double().numpy())
+    m = metrics(t2np(logp), ref_lp)
+    assert m["finite"] and m["max_abs"] <= LOGP_MAX_ABS, m
+    assert metrics(t2np(lse), ref_lse)["max_abs"] <= LOGP_MAX_ABS
+    assert torch.equal(logp, logp2)
+    for d in (dz, dz2):
+        md = metrics(t2np(d), ref_dz)
+        assert md["finite"] and md["rel_l2"] <= DZ_REL_L2, md
+    # sum_v dz = 0 per row (up to bf16 rounding of dz)
+    assert t2np(dz).sum(1).__abs__().max() < 1e-2 * max(1.0, np.abs(w.numpy()).max())
+
+
+@pytest.mark.gpu
+def test_logprob_inplace_strided_and_bad_target(cuda_ok):
+    n, V, S = 8, 1000, 1024
+    z, t = logits_inputs(n, V, seed=3)
+    big = torch.zeros(n, S, dtype=torch.bfloat16)
+    big[:, :V] = z
+    bc = big.cuda()
+    view = bc[:, :V]
+    t_bad = t.clone()
+    t_bad[2] = V  # out of range -> NaN for that row
+    w = torch.ones(n)
+    logp, lse = ops.logprob(view, t_bad.cuda())
+    lp = t2np(logp)
+    assert np.isnan(lp[2]) and np.isfinite(np.delete(lp, 2)).all()
+    ref_lp, _ = olp.logprob(z, t.long())
+    assert np.abs(np.delete(lp, 2) - np.delete(ref_lp, 2)).max() <= LOGP_MAX_ABS
+    # in-place gradient over the strided view
+    ops.logprob(view, t.cuda(), dlogp=w.cuda(), dlogits=view)
+    torch.cuda.synchronize()
+    ref_dz = olp.logprob_grad(z, t.long(), w.double().numpy())
+    assert metrics(t2np(view), ref_dz)["rel_l2"] <= DZ_REL_L2
+    assert torch.all(bc[:, V:] == 0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("clip", [False, True])
+def test_dipo_kernels_vs_oracle(cuda_ok, clip):
+    n_groups, G = 4, 8
+    g = torch.Generator().manual_seed(11)
+    lens = torch.randint(1, 40, (n_groups * G,), generator=g).tolist()
+    rewards, group_of_traj, traj_of_token = rl_batch(n_groups, G, lens, seed=2)
+    n_tok = traj_of_token.numel()
+    logp = -torch.rand(n_tok, generator=g, dtype=torch.float64) * 3
+    old = logp.clone()
+    if clip:
+        old += torch.randn(n_tok, generator=g, dtype=torch.float64) * 0.3
+    loss, dl, st = odipo.dipo_loss(logp.numpy(), old.numpy(), traj_of_token.numpy(), rewards.numpy(),
+                                   group_of_traj.numpy())
+    lp32, old32 = logp.float(), old.float()
+    # the kernel computes rho from fp32 inputs; feed the oracle the same fp32 values
+    loss32, dl32, _ = odipo.dipo_loss(lp32.double().numpy(), old32.double().numpy(), traj_of_token.numpy(),
+                                      rewards.numpy(), group_of_traj.numpy())
+    cu = lambda x, dt: x.to(dt).cuda()
+    gloss, gdl, parts = bdipo.dipo_loss(cu(lp32, torch.float32), cu(old32, torch.float32),
+                                        cu(traj_of_token, torch.int32), cu(rewards, torch.float32),
+                                        cu(group_of_traj, torch.int32), cu(torch.tensor(lens), torch.int32),
+                                        n_groups)
+    torch.cuda.synchronize()
+    assert abs(gloss.item() - loss32) < 1e-6 * max(1.0, abs(loss32))
+    np.testing.assert_allclose(t2np(gdl), dl32, rtol=1e-5, atol=1e-9)
+    assert parts[1].item() == n_tok
+    if not clip:
+        np.testing.assert_allclose(t2np(gdl), dl, rtol=1e-5, atol=1e-9)
+        assert parts[2].item() == 0

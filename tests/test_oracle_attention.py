@@ -215,3 +215,20 @@ def test_backward_slice_matches_full():
     np.testing.assert_allclose(sdk, dk[1, :, 1], atol=0)
     np.testing.assert_allclose(so, o[1, :, 2:4], atol=1e-14)
     np.testing.assert_allclose(slse, lse[1, 2:4], atol=1e-14)
+
+
+def test_backward_rows_sum_to_full():
+    """backward_rows over a partition of the rows adds up to backward_slice."""
+    prob = Problem(1, 4, 12, 4, 2, 1, 8)
+    q, k, v, do = _inputs(prob, 71)
+    dq, dk, dv, _, _ = attention.backward_slice(prob, q, k, v, do, 0, 0)
+    acc_k = np.zeros_like(dk)
+    acc_v = np.zeros_like(dv)
+    for h in range(2):
+        for rows in (np.arange(0, 13), np.arange(13, prob.ntot)):
+            dqr, dkp, dvp = attention.backward_rows(prob, q, k, v, do, 0, h, rows)
+            np.testing.assert_allclose(dqr, dq[rows, h], atol=1e-13)
+            acc_k += dkp
+            acc_v += dvp
+    np.testing.assert_allclose(acc_k, dk, atol=1e-12)
+    np.testing.assert_allclose(acc_v, dv, atol=1e-12)
