@@ -20,8 +20,7 @@ WsLayout ws_layout(const bd_problem& p, int backward) {
   if (backward) {
     w.dsum_off = off;  // tile-major log2-LSE and D vectors
     off = align256(off + bwd_vec_floats(p, g) * sizeof(float));
-    w.dq_off = off;
-    off = align256(off + (size_t)p.batch * g.N * p.n_q_heads * p.head_dim * sizeof(float));
+    w.dq_off = off;  // dQ is accumulated in TMEM: no fp32 accumulator needed
   }
   w.total = off;
   return w;

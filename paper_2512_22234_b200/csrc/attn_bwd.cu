@@ -5,23 +5,27 @@
 //   dS = P o (dP - D) with D_i = rowsum(dO_i o O_i),
 //   dQ = scale dS K, dK = scale dS^T Q (dK, dV summed over the q-heads of a group).
 //
-// Kernels:
-//  1. bwd_pre:   D and log2-domain LSE in a tile-major workspace layout (so a
-//                q-tile's 128 values are one aligned 512 B bulk copy), and
-//                zero the fp32 dQ accumulator.
-//  2. bwd_main:  one CTA per (k-tile, sequence, kv head), visiting only the
-//                q-tiles of the tile map's column list (EMPTY tiles never
-//                loaded), for every q-head of the group.  K and V stay in smem;
-//                Q, dO, LSE, D stream through a 2-stage TMA ring.  TMEM holds
-//                S^T [0,128), dP^T [128,256), dV and dK accumulators; P^T (bf16)
-//                overwrites S^T in place and feeds dV += P^T dO from TMEM; dS^T
-//                (bf16) goes to smem and feeds both dK += dS^T Q (K-major A) and
-//                dQ = dS K (MN-major A), the latter into the dP^T columns, from
-//                where the compute warps reduce it into the fp32 dQ accumulator
-//                with vector atomics.
-//  3. bwd_post:  dQ = bf16(scale dQ_acc).
-// Warps 0-7: compute (two warpgroups split the 128 q columns of a tile; a
-// thread owns one key row = one TMEM lane); warp 8: TMA; warp 9: MMA issuer.
+// Three launches, no atomics:
+//  1. bwd_pre:  D and the log2-domain LSE in a tile-major workspace layout
+//               (a q-tile's 128 values form one aligned 512 B bulk copy).
+//  2. dkdv:     one CTA per (k-tile, sequence, kv head), visiting only the
+//               q-tiles of the tile map's column list (EMPTY tiles never
+//               loaded), for every q-head of the group.  K, V stay in smem;
+//               Q, dO, LSE, D stream through a 2-stage TMA ring.  TMEM:
+//               S^T [0,128), dP^T [128,256), dV, dK accumulators.  P^T (bf16)
+//               overwrites S^T in place and feeds dV += P^T dO from TMEM; dS^T
+//               (bf16) goes to smem and feeds dK += dS^T Q.  MMA order per
+//               iteration: dV(i), dP^T(i+1), S^T(i+1), dK(i) (in two K-halves)
+//               so the compute of i+1 overlaps dK(i).
+//  3. dq:       one CTA per (q-tile, sequence, q-head), visiting the tile map's
+//               row list: S = QK^T (double-buffered in TMEM), dP = dO V^T,
+//               dS (bf16) overwrites S and feeds dQ += dS K from TMEM.  The
+//               compute of tile j overlaps S(j+1) and dQ(j-1).
+// dQ is therefore accumulated in TMEM and written once (deterministic), at
+// the price of recomputing S and dP per (q-tile, k-tile) pair -- cheaper on
+// B200 than 64 KB of fp32 L2 reductions per tile pair (profiles/r01).
+// Compute warps: two warpgroups split the 128 columns of a tile; a thread owns
+// one TMEM lane (a key row in dkdv, a query row in dq).
 #include "sm100.cuh"
 #include "tma_host.h"
 #include "tilemap.cuh"
@@ -74,16 +78,32 @@ __global__ void zero_kernel(float4* __restrict__ p, size_t n4) {
     p[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-__global__ void dq_convert_kernel(const float4* __restrict__ acc, uint2* __restrict__ dq, size_t n4, float scale) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
-    const float4 v = acc[i];
-    dq[i] = make_uint2(pack_bf16x2(v.x * scale, v.y * scale), pack_bf16x2(v.z * scale, v.w * scale));
+struct BwdArgs {
+  const int* map;
+  const float* lse2_t;
+  const float* dsum_t;
+  __nv_bfloat16* dq;
+  __nv_bfloat16* dk;
+  __nv_bfloat16* dv;
+  int batch, n_q_heads, n_kv_heads, group, N;
+  Geom g;
+  float scale, scale_log2;
+};
+
+__device__ __forceinline__ void store_row_bf16(__nv_bfloat16* dst, const uint32_t* v, float mul, bool ok) {
+  uint32_t pk[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(__uint_as_float(v[2 * j]) * mul, __uint_as_float(v[2 * j + 1]) * mul);
+  if (ok) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) d4[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
   }
 }
 
-// ------------------------------------------------------------------ main
+// ================================================================== dK/dV
 template <int D>
-struct BwdCfg {
+struct DkdvCfg {
   static constexpr int kTileBytes = 128 * D * 2;
   static constexpr int kStages = 2;
   static constexpr int kComputeWarps = 8;
@@ -92,7 +112,6 @@ struct BwdCfg {
   static constexpr int kThreads = 320;
   static constexpr int kColS = 0, kColDP = 128, kColDV = 256, kColDK = 256 + D;
   static constexpr uint32_t kTmemCols = 512;
-  // smem: K, V, dS^T, stages x {Q, dO}, stages x {lse2[128], dsum[128]}, barriers
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kTileBytes;
   static constexpr int kOffDS = 2 * kTileBytes;
@@ -102,29 +121,17 @@ struct BwdCfg {
   static constexpr int kOffVec = kOffStage + kStages * kStageBytes;
   static constexpr int kVecBytes = 2 * 128 * 4;
   static constexpr int kOffBar = kOffVec + kStages * kVecBytes;
-  // kv_full, qd_full[2], qd_empty[2], s_full, dp_full, compute_done, dv_done, dq_full, dq_empty, acc_done
-  static constexpr int kNumBars = 1 + 2 * kStages + 7;
+  // kv_full, qd_full[2], qd_empty[2], s_full, dp_full, compute_done, dv_done, dka_done, dkb_done, acc_done
+  static constexpr int kNumBars = 1 + 2 * kStages + 8;
   static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16;
 };
 
-struct BwdArgs {
-  const int* map;
-  const float* lse2_t;
-  const float* dsum_t;
-  float* dq_acc;
-  __nv_bfloat16* dk;
-  __nv_bfloat16* dv;
-  int batch, n_q_heads, n_kv_heads, group, N;
-  Geom g;
-  float scale, scale_log2;
-};
-
 template <int D>
-__global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
-    attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
-                    const BwdArgs a) {
-  using C = BwdCfg<D>;
+__global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
+    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                         const BwdArgs a) {
+  using C = DkdvCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sK = smem + C::kOffK;
   uint8_t* sV = smem + C::kOffV;
@@ -137,16 +144,15 @@ __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
   uint64_t* dp_full = s_full + 1;
   uint64_t* compute_done = dp_full + 1;
   uint64_t* dv_done = compute_done + 1;
-  uint64_t* dq_full = dv_done + 1;
-  uint64_t* dq_empty = dq_full + 1;
-  uint64_t* acc_done = dq_empty + 1;
+  uint64_t* dka_done = dv_done + 1;
+  uint64_t* dkb_done = dka_done + 1;
+  uint64_t* acc_done = dkb_done + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   const Geom& g = a.g;
   if ((smem_u32(smem) & 1023u) != 0) __trap();
 
-  // ---- work unit: LPT rank of the k-tile, then (sequence, kv head)
   const int per_tile = a.batch * a.n_kv_heads;
   const int rank = blockIdx.x / per_tile;
   const int rem = blockIdx.x - rank * per_tile;
@@ -171,8 +177,8 @@ __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
     mbar_init(dp_full, 1);
     mbar_init(compute_done, C::kComputeWarps);
     mbar_init(dv_done, 1);
-    mbar_init(dq_full, 1);
-    mbar_init(dq_empty, C::kComputeWarps);
+    mbar_init(dka_done, 1);
+    mbar_init(dkb_done, 1);
     mbar_init(acc_done, 1);
     fence_barrier_init();
   }
@@ -200,7 +206,7 @@ __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
         uint8_t* sq = smem + C::kOffStage + stage * C::kStageBytes;
         for (int kb = 0; kb < D / 64; ++kb) {
           tma_load_4d(sq + kb * 16384, &tmQ, &qd_full[stage], kb * 64, h, q0, b);
-          tma_load_4d(sq + C::kTileBytes + kb * 16384, &tmO, &qd_full[stage], kb * 64, h, q0, b);
+          tma_load_4d(sq + C::kTileBytes + kb * 16384, &tmDO, &qd_full[stage], kb * 64, h, q0, b);
         }
         const size_t vec = (((size_t)b * a.n_q_heads + h) * g.NT + qt) * kTileRows;
         float* sv = reinterpret_cast<float*>(smem + C::kOffVec + stage * C::kVecBytes);
@@ -217,10 +223,10 @@ __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
     if (elect_one() && n_it > 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);  // S^T, dP^T
       constexpr uint32_t idesc_kv = umma_idesc_bf16(128, D, false, true);    // dV, dK: B MN-major
-      constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, true, true);      // dQ: A, B MN-major
       const uint32_t kaddr = smem_u32(sK), vaddr = smem_u32(sV), dsaddr = smem_u32(sDS);
-      auto issue_s = [&](int stage) {
-        const uint32_t qaddr = smem_u32(smem + C::kOffStage + stage * C::kStageBytes);
+      auto stage_addr = [&](int st) { return smem_u32(smem + C::kOffStage + st * C::kStageBytes); };
+      auto issue_s = [&](int st) {  // S^T = K Q^T
+        const uint32_t qaddr = stage_addr(st);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
@@ -229,8 +235,8 @@ __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
         }
         umma_commit(s_full);
       };
-      auto issue_dp = [&](int stage) {
-        const uint32_t doaddr = smem_u32(smem + C::kOffStage + stage * C::kStageBytes + C::kTileBytes);
+      auto issue_dp = [&](int st) {  // dP^T = V dO^T
+        const uint32_t doaddr = stage_addr(st) + C::kTileBytes;
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
@@ -247,8 +253,11 @@ __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int i = 0; i < n_it; ++i) {
-        const uint32_t qaddr = smem_u32(smem + C::kOffStage + stage * C::kStageBytes);
+        const uint32_t qaddr = stage_addr(stage);
         const uint32_t doaddr = qaddr + C::kTileBytes;
+        const int nstage = stage + 1 == C::kStages ? 0 : stage + 1;
+        const uint32_t nphase = stage + 1 == C::kStages ? phase ^ 1 : phase;
+        const bool has_next = i + 1 < n_it;
         mbar_wait(compute_done, i & 1);
         tc_fence_after();
         // dV += P^T dO   (A = P^T in TMEM: q 0..63 at cols [0,32), q 64..127 at [64,96))
@@ -257,31 +266,25 @@ __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
           umma_ts(tbase + C::kColDV, tbase + C::kColS + (k < 4 ? k * 8 : 64 + (k - 4) * 8),
                   umma_desc_sw128(doaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
         umma_commit(dv_done);
-        // dK += dS^T Q   (A = dS^T smem K-major, B = Q MN-major)
+        if (has_next) {
+          mbar_wait(&qd_full[nstage], nphase);
+          tc_fence_after();
+          issue_dp(nstage);               // dP^T region was read by compute(i)
+          mbar_wait(dv_done, i & 1);      // P^T(i) consumed -> S^T region free
+          tc_fence_after();
+          issue_s(nstage);
+        }
+        // dK += dS^T Q   (A = dS^T smem K-major, B = Q MN-major), q-halves committed separately
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
+        for (int k = 0; k < 8; ++k) {
           umma_ss(tbase + C::kColDK, umma_desc_sw128(dsaddr + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024),
                   umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
-        // dQ = dS K      (A = dS^T smem read MN-major, B = K MN-major) -> dP^T columns
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          umma_ss(tbase + C::kColDP, umma_desc_sw128(dsaddr + k * 2048, 16384, 1024),
-                  umma_desc_sw128(kaddr + k * 2048, 16384, 1024), idesc_q, k > 0);
-        umma_commit(dq_full);
+          if (k == 3) umma_commit(dka_done);
+        }
+        umma_commit(dkb_done);
         umma_commit(&qd_empty[stage]);
-        if (++stage == C::kStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-        if (i + 1 < n_it) {
-          mbar_wait(dv_done, i & 1);  // P^T(i) consumed -> S^T columns free
-          mbar_wait(&qd_full[stage], phase);
-          tc_fence_after();
-          issue_s(stage);
-          mbar_wait(dq_empty, i & 1);  // dQ(i) drained -> dP^T columns free
-          tc_fence_after();
-          issue_dp(stage);
-        }
+        stage = nstage;
+        phase = nphase;
       }
       umma_commit(acc_done);
     }
@@ -291,23 +294,23 @@ __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
     const int r = (warp & 3) * 32 + lane;     // key row within the tile == TMEM lane
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const float sl2 = a.scale_log2;
-    const int kpos = k0 + r;                  // packed key column of this thread
+    const int kpos = k0 + r;
+    uint64_t* my_dk_done = wg ? dkb_done : dka_done;
     int stage = 0;
     uint32_t phase = 0;
     for (int i = 0; i < n_it; ++i) {
       const int ent = ents[i / a.group];
       const int qt = entry_tile(ent);
-      const int h = kvh * a.group + (i % a.group);
       const int q0 = tile_start(g, qt), q1 = tile_end(g, qt), qseg = tile_seg(g, qt);
       const bool need_mask = entry_kind(ent) == kKindPartial || (q1 - q0) < 128 || (k1 - k0) < 128;
       const float* sv = reinterpret_cast<const float*>(smem + C::kOffVec + stage * C::kVecBytes);
-      mbar_wait(&qd_full[stage], phase);  // LSE / D of this q-tile landed
+      mbar_wait(&qd_full[stage], phase);
       mbar_wait(s_full, i & 1);
       mbar_wait(dp_full, i & 1);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const int cb = wg * 64 + c * 32;  // first q column of this chunk
+        const int cb = wg * 64 + c * 32;
         uint32_t sr[32], dr[32];
         tmem_ld32(tbase + lane_off + C::kColS + cb, sr);
         tmem_ld32(tbase + lane_off + C::kColDP + cb, dr);
@@ -333,11 +336,10 @@ __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(pv[2 * j], pv[2 * j + 1]);
-        // P^T (bf16) into this warpgroup's own S^T columns (already read)
         tmem_st16(tbase + lane_off + C::kColS + wg * 64 + c * 16, pk);
-        // dS^T (bf16) into smem, K-major rows = keys, block wg = q half
 #pragma unroll
         for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(ds[2 * j], ds[2 * j + 1]);
+        if (c == 0 && i > 0) mbar_wait(my_dk_done, (i - 1) & 1);  // dK(i-1) has read this dS^T half
         uint8_t* dsrow = sDS + wg * 16384;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -349,29 +351,6 @@ __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(compute_done);
-      // ---- dQ(i): TMEM (lane = q row) -> fp32 atomics
-      mbar_wait(dq_full, i & 1);
-      tc_fence_after();
-      {
-        const int qrow = q0 + r;
-        float* dst = a.dq_acc + (((size_t)b * a.N + qrow) * a.n_q_heads + h) * D + wg * (D / 2);
-        const bool ok = qrow < q1;
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          uint32_t v[32];
-          tmem_ld32(tbase + lane_off + C::kColDP + wg * (D / 2) + 32 * c, v);
-          tmem_ld_wait();
-          if (ok) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              red_add_v4(dst + 32 * c + 4 * u, __uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1]),
-                         __uint_as_float(v[4 * u + 2]), __uint_as_float(v[4 * u + 3]));
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dq_empty);
       if (++stage == C::kStages) {
         stage = 0;
         phase ^= 1;
@@ -387,22 +366,18 @@ __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
 #pragma unroll
     for (int which = 0; which < 2; ++which) {
       const uint32_t col = (which ? C::kColDK : C::kColDV) + wg * (D / 2);
-      const float mul = which ? a.scale : 1.f;
+      const float mul = n_it > 0 ? (which ? a.scale : 1.f) : 0.f;
       __nv_bfloat16* out = (which ? a.dk : a.dv) + orow;
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
         uint32_t v[32];
         tmem_ld32(tbase + lane_off + col + 32 * c, v);
         tmem_ld_wait();
-        uint32_t pk[16];
+        if (n_it == 0) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          pk[j] = n_it > 0 ? pack_bf16x2(__uint_as_float(v[2 * j]) * mul, __uint_as_float(v[2 * j + 1]) * mul) : 0u;
-        if (ok) {
-          uint4* dst = reinterpret_cast<uint4*>(out + 32 * c);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) dst[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          for (int j = 0; j < 32; ++j) v[j] = 0u;
         }
+        store_row_bf16(out + 32 * c, v, mul, ok);
       }
     }
   }
@@ -411,18 +386,262 @@ __global__ void __launch_bounds__(BwdCfg<D>::kThreads, 1)
   if (warp == 0) tmem_dealloc<C::kTmemCols>(tbase);
 }
 
+// ===================================================================== dQ
+template <int D>
+struct DqCfg {
+  static constexpr int kTileBytes = 128 * D * 2;
+  static constexpr int kStages = 4;  // K/V ring (K(j), V(j) alternate)
+  static constexpr int kComputeWarps = 8;
+  static constexpr int kTmaWarp = 8;
+  static constexpr int kMmaWarp = 9;
+  static constexpr int kThreads = 320;
+  static constexpr int kColS0 = 0, kColS1 = 128, kColDP = 256, kColDQ = 384;
+  static constexpr uint32_t kTmemCols = 512;
+  static constexpr int kOffQ = 0;
+  static constexpr int kOffDO = kTileBytes;
+  static constexpr int kOffRing = 2 * kTileBytes;
+  static constexpr int kOffBar = kOffRing + kStages * kTileBytes;
+  // q_full, kv_full[S], kv_empty[S], s_full[2], dp_full, compute_done, dq_done, acc_done
+  static constexpr int kNumBars = 1 + 2 * kStages + 6;
+  static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16;
+};
+
+template <int D>
+__global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
+    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                       const BwdArgs a) {
+  using C = DqCfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sQ = smem + C::kOffQ;
+  uint8_t* sDO = smem + C::kOffDO;
+  uint8_t* sRing = smem + C::kOffRing;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + C::kStages;
+  uint64_t* s_full = kv_empty + C::kStages;  // [2]
+  uint64_t* dp_full = s_full + 2;
+  uint64_t* compute_done = dp_full + 1;
+  uint64_t* dq_done = compute_done + 1;
+  uint64_t* acc_done = dq_done + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
+
+  const int warp = (int)warp_id(), lane = (int)lane_id();
+  const Geom& g = a.g;
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
+
+  const int per_tile = a.batch * a.n_q_heads;
+  const int rank = blockIdx.x / per_tile;
+  const int rem = blockIdx.x - rank * per_tile;
+  const int b = rem / a.n_q_heads;
+  const int h = rem - b * a.n_q_heads;
+  const int kvh = h / a.group;
+  const MapView mv{const_cast<int*>(a.map), g.NT, map_capacity(g)};
+  const int qt = mv.fwd_order()[rank];
+  const int e0 = mv.row_ptr()[qt];
+  const int n_kt = mv.row_ptr()[qt + 1] - e0;
+  const int* ents = mv.row_ent() + e0;
+  const int q0 = tile_start(g, qt), q1 = tile_end(g, qt), qseg = tile_seg(g, qt);
+
+  if (warp == 0) tmem_alloc<C::kTmemCols>(tslot);
+  if (warp == C::kTmaWarp && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    mbar_init(&s_full[0], 1);
+    mbar_init(&s_full[1], 1);
+    mbar_init(dp_full, 1);
+    mbar_init(compute_done, C::kComputeWarps);
+    mbar_init(dq_done, 1);
+    mbar_init(acc_done, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == C::kTmaWarp) {
+    // ================================================================ TMA
+    if (elect_one()) {
+      mbar_expect_tx(q_full, 2 * C::kTileBytes);
+      for (int kb = 0; kb < D / 64; ++kb) {
+        tma_load_4d(sQ + kb * 16384, &tmQ, q_full, kb * 64, h, q0, b);
+        tma_load_4d(sDO + kb * 16384, &tmDO, q_full, kb * 64, h, q0, b);
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int j = 0; j < n_kt; ++j) {
+        const int k0 = tile_start(g, entry_tile(ents[j]));
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv) {
+          mbar_wait(&kv_empty[stage], phase ^ 1);
+          mbar_expect_tx(&kv_full[stage], C::kTileBytes);
+          uint8_t* dst = sRing + stage * C::kTileBytes;
+          for (int kb = 0; kb < D / 64; ++kb)
+            tma_load_4d(dst + kb * 16384, kv ? &tmV : &tmK, &kv_full[stage], kb * 64, kvh, k0, b);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == C::kMmaWarp) {
+    // ================================================================ MMA
+    if (elect_one()) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);  // S = Q K^T, dP = dO V^T
+      constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, false, true);     // dQ += dS K (B MN-major)
+      const uint32_t qaddr = smem_u32(sQ), doaddr = smem_u32(sDO);
+      // ring slot of K(j) is 2j mod S, of V(j) is 2j+1 mod S; phase = (2j / S) & 1 ...
+      auto slot = [&](int idx) { return idx % C::kStages; };
+      auto ph = [&](int idx) { return (uint32_t)((idx / C::kStages) & 1); };
+      auto ring = [&](int idx) { return smem_u32(sRing + slot(idx) * C::kTileBytes); };
+      auto issue_s = [&](int j) {
+        const uint32_t kaddr = ring(2 * j);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+          umma_ss(tbase + ((j & 1) ? C::kColS1 : C::kColS0), umma_desc_sw128(qaddr + off, 16, 1024),
+                  umma_desc_sw128(kaddr + off, 16, 1024), idesc_s, k > 0);
+        }
+        umma_commit(&s_full[j & 1]);
+      };
+      auto issue_dp = [&](int j) {
+        const uint32_t vaddr = ring(2 * j + 1);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+          umma_ss(tbase + C::kColDP, umma_desc_sw128(doaddr + off, 16, 1024),
+                  umma_desc_sw128(vaddr + off, 16, 1024), idesc_s, k > 0);
+        }
+        umma_commit(dp_full);
+        umma_commit(&kv_empty[slot(2 * j + 1)]);  // V(j) consumed
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&kv_full[slot(0)], ph(0));
+      tc_fence_after();
+      issue_s(0);
+      mbar_wait(&kv_full[slot(1)], ph(1));
+      tc_fence_after();
+      issue_dp(0);
+      for (int j = 0; j < n_kt; ++j) {
+        if (j + 1 < n_kt) {
+          mbar_wait(&kv_full[slot(2 * j + 2)], ph(2 * j + 2));
+          if (j >= 1) mbar_wait(dq_done, (j - 1) & 1);  // dS(j-1) in S[(j+1)&1] consumed
+          tc_fence_after();
+          issue_s(j + 1);
+        }
+        mbar_wait(compute_done, j & 1);
+        tc_fence_after();
+        if (j + 1 < n_kt) {
+          mbar_wait(&kv_full[slot(2 * j + 3)], ph(2 * j + 3));
+          tc_fence_after();
+          issue_dp(j + 1);  // dP region was read by compute(j)
+        }
+        // dQ += dS(j) K(j): A = dS bf16 in S[j&1] (keys 0..63 at +0, 64..127 at +64)
+        const uint32_t sbase = tbase + ((j & 1) ? C::kColS1 : C::kColS0);
+        const uint32_t kaddr = ring(2 * j);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          umma_ts(tbase + C::kColDQ, sbase + (k < 4 ? k * 8 : 64 + (k - 4) * 8),
+                  umma_desc_sw128(kaddr + k * 2048, 16384, 1024), idesc_q, (j > 0 || k > 0) ? 1u : 0u);
+        umma_commit(dq_done);
+        umma_commit(&kv_empty[slot(2 * j)]);  // K(j) consumed
+      }
+      umma_commit(acc_done);
+    }
+  } else {
+    // ========================================================== compute
+    const int wg = warp >> 2;
+    const int r = (warp & 3) * 32 + lane;  // query row within the tile == TMEM lane
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const float sl2 = a.scale_log2;
+    const int row = q0 + r;
+    int lo0, hi0, lo1, hi1;
+    row_interval(g, qseg, row, 0, lo0, hi0);
+    row_interval(g, qseg, row, 1, lo1, hi1);
+    const size_t vslot = (((size_t)b * a.n_q_heads + h) * g.NT + qt) * kTileRows + r;
+    const float lse2 = a.lse2_t[vslot];
+    const float dsum = a.dsum_t[vslot];
+    for (int j = 0; j < n_kt; ++j) {
+      const int ent = ents[j];
+      const int kt = entry_tile(ent);
+      const int k0 = tile_start(g, kt), k1 = tile_end(g, kt);
+      const bool need_mask = entry_kind(ent) == kKindPartial || (k1 - k0) < 128;
+      const bool xt = tile_seg(g, kt) != 0;
+      const int lo = (xt ? lo1 : lo0) - k0;
+      const int hi = min(xt ? hi1 : hi0, k1) - k0;
+      const uint32_t sbase = tbase + lane_off + ((j & 1) ? C::kColS1 : C::kColS0);
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      mbar_wait(dp_full, j & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int cb = wg * 64 + c * 32;
+        uint32_t sr[32], dr[32];
+        tmem_ld32(sbase + cb, sr);
+        tmem_ld32(tbase + lane_off + C::kColDP + cb, dr);
+        tmem_ld_wait();
+        float ds[32];
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+          const float p = ex2_approx(fmaf(__uint_as_float(sr[jj]), sl2, -lse2));
+          ds[jj] = p * (__uint_as_float(dr[jj]) - dsum);
+        }
+        if (need_mask) {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) ds[jj] = (cb + jj >= lo && cb + jj < hi) ? ds[jj] : 0.f;
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) pk[jj] = pack_bf16x2(ds[2 * jj], ds[2 * jj + 1]);
+        tmem_st16(sbase + wg * 64 + c * 16, pk);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(compute_done);
+    }
+    // ---- epilogue: dQ = scale * acc -> bf16
+    mbar_wait(acc_done, 0);
+    tc_fence_after();
+    const bool ok = row < q1;
+    __nv_bfloat16* out = a.dq + (((size_t)b * a.N + row) * a.n_q_heads + h) * D + wg * (D / 2);
+#pragma unroll
+    for (int c = 0; c < D / 64; ++c) {
+      uint32_t v[32];
+      tmem_ld32(tbase + lane_off + C::kColDQ + wg * (D / 2) + 32 * c, v);
+      tmem_ld_wait();
+      store_row_bf16(out + 32 * c, v, a.scale, ok);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<C::kTmemCols>(tbase);
+}
+
+template <typename K>
+int set_smem(K kernel, int bytes, bool& done) {
+  if (done) return BD_OK;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(bwd)");
+  done = true;
+  return BD_OK;
+}
+
 template <int D>
 int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, const void* o,
                const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, float* vec_ws,
-               float* dq_acc, cudaStream_t stream) {
-  using C = BwdCfg<D>;
+               cudaStream_t stream) {
   const int Hq = p.n_q_heads;
   const size_t nvec = (size_t)p.batch * Hq * g.NT * kTileRows;
   float* lse2_t = vec_ws;
   float* dsum_t = vec_ws + nvec;
-  const size_t nacc = (size_t)p.batch * g.N * Hq * D;
-  // 1. zero the dQ accumulator and the padded vectors; D and log2 LSE
-  zero_kernel<<<1184, 256, 0, stream>>>(reinterpret_cast<float4*>(dq_acc), nacc / 4);
+  // 1. preprocess: D and log2 LSE, tile-major (pad rows zeroed)
   zero_kernel<<<296, 256, 0, stream>>>(reinterpret_cast<float4*>(vec_ws), 2 * nvec / 4);
   {
     dim3 grid((g.N + 3) / 4, p.batch * Hq);
@@ -430,23 +649,19 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
                                                  reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2_t, dsum_t,
                                                  g.N, Hq, g);
   }
-  // 2. main
-  CUtensorMap tmQ, tmK, tmV, tmO;
+  CUtensorMap tmQ, tmK, tmV, tmDO;
   if (!make_qkv_tmap(&tmQ, q, p.batch, g.N, Hq, D) || !make_qkv_tmap(&tmK, k, p.batch, g.N, p.n_kv_heads, D) ||
-      !make_qkv_tmap(&tmV, v, p.batch, g.N, p.n_kv_heads, D) || !make_qkv_tmap(&tmO, dout, p.batch, g.N, Hq, D))
+      !make_qkv_tmap(&tmV, v, p.batch, g.N, p.n_kv_heads, D) || !make_qkv_tmap(&tmDO, dout, p.batch, g.N, Hq, D))
     return set_error(BD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(bwd)");
-    attr = true;
-  }
+  static bool attr_kv = false, attr_q = false;
+  int rc = set_smem(attn_bwd_dkdv_kernel<D>, DkdvCfg<D>::kSmemBytes, attr_kv);
+  if (rc) return rc;
+  if ((rc = set_smem(attn_bwd_dq_kernel<D>, DqCfg<D>::kSmemBytes, attr_q))) return rc;
   BwdArgs a;
   a.map = map;
   a.lse2_t = lse2_t;
   a.dsum_t = dsum_t;
-  a.dq_acc = dq_acc;
+  a.dq = reinterpret_cast<__nv_bfloat16*>(dq);
   a.dk = reinterpret_cast<__nv_bfloat16*>(dk);
   a.dv = reinterpret_cast<__nv_bfloat16*>(dv);
   a.batch = p.batch;
@@ -457,15 +672,18 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   a.g = g;
   a.scale = scale_of(p);
   a.scale_log2 = a.scale * kLog2e;
-  const long long grid = (long long)g.NT * p.batch * p.n_kv_heads;
-  attn_bwd_kernel<D><<<(unsigned)grid, C::kThreads, C::kSmemBytes, stream>>>(tmQ, tmK, tmV, tmO, a);
-  note_launches(5);  // zero x2, pre, main, convert (below)
-  int rc = check_cuda(cudaGetLastError(), "attn_bwd_kernel launch");
-  if (rc) return rc;
-  // 3. dQ = bf16(scale * acc)
-  dq_convert_kernel<<<1184, 256, 0, stream>>>(reinterpret_cast<const float4*>(dq_acc), reinterpret_cast<uint2*>(dq),
-                                              nacc / 4, a.scale);
-  return check_cuda(cudaGetLastError(), "dq_convert launch");
+  // 2. dK, dV
+  const long long grid_kv = (long long)g.NT * p.batch * p.n_kv_heads;
+  attn_bwd_dkdv_kernel<D><<<(unsigned)grid_kv, DkdvCfg<D>::kThreads, DkdvCfg<D>::kSmemBytes, stream>>>(
+      tmQ, tmK, tmV, tmDO, a);
+  if ((rc = check_cuda(cudaGetLastError(), "attn_bwd_dkdv_kernel launch"))) return rc;
+  // 3. dQ
+  const long long grid_q = (long long)g.NT * p.batch * Hq;
+  if (grid_q > 0x7FFFFFFF) return set_error(BD_ERR_UNSUPPORTED, "grid too large");
+  attn_bwd_dq_kernel<D><<<(unsigned)grid_q, DqCfg<D>::kThreads, DqCfg<D>::kSmemBytes, stream>>>(tmQ, tmK, tmV,
+                                                                                               tmDO, a);
+  note_launches(4);  // zero, pre, dkdv, dq
+  return check_cuda(cudaGetLastError(), "attn_bwd_dq_kernel launch");
 }
 
 }  // namespace
@@ -476,11 +694,9 @@ size_t bwd_vec_floats(const bd_problem& p, const Geom& g) {
 
 int run_attn_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, const void* o,
                  const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, float* vec_ws,
-                 float* dq_acc, cudaStream_t stream) {
-  if (p.head_dim == 128)
-    return launch_bwd<128>(p, g, q, k, v, o, lse, dout, dq, dk, dv, map, vec_ws, dq_acc, stream);
-  if (p.head_dim == 64)
-    return launch_bwd<64>(p, g, q, k, v, o, lse, dout, dq, dk, dv, map, vec_ws, dq_acc, stream);
+                 float* /*unused*/, cudaStream_t stream) {
+  if (p.head_dim == 128) return launch_bwd<128>(p, g, q, k, v, o, lse, dout, dq, dk, dv, map, vec_ws, stream);
+  if (p.head_dim == 64) return launch_bwd<64>(p, g, q, k, v, o, lse, dout, dq, dk, dv, map, vec_ws, stream);
   return set_error(BD_ERR_UNSUPPORTED, "head_dim %d not in {64, 128}", p.head_dim);
 }
 
