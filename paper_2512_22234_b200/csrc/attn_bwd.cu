@@ -252,6 +252,10 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
       issue_dp(0);
       int stage = 0;
       uint32_t phase = 0;
+      // Per iteration, after compute(i): S^T(i+1) (S region is free: compute(i)
+      // read it in phase 1), dV(i) (P^T(i) lives in the dP region), dK(i) first
+      // q-half, dP^T(i+1) once dV(i) has consumed P^T(i), dK(i) second half.
+      // compute(i+1) phase 1 (exp) overlaps dV/dK; phase 2 needs dP^T(i+1).
       for (int i = 0; i < n_it; ++i) {
         const uint32_t qaddr = stage_addr(stage);
         const uint32_t doaddr = qaddr + C::kTileBytes;
@@ -260,27 +264,32 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
         const bool has_next = i + 1 < n_it;
         mbar_wait(compute_done, i & 1);
         tc_fence_after();
-        // dV += P^T dO   (A = P^T in TMEM: q 0..63 at cols [0,32), q 64..127 at [64,96))
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          umma_ts(tbase + C::kColDV, tbase + C::kColS + (k < 4 ? k * 8 : 64 + (k - 4) * 8),
-                  umma_desc_sw128(doaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
-        umma_commit(dv_done);
         if (has_next) {
           mbar_wait(&qd_full[nstage], nphase);
           tc_fence_after();
-          issue_dp(nstage);               // dP^T region was read by compute(i)
-          mbar_wait(dv_done, i & 1);      // P^T(i) consumed -> S^T region free
-          tc_fence_after();
           issue_s(nstage);
         }
+        // dV += P^T dO   (A = P^T in TMEM: q 0..63 at dP cols [0,32), q 64..127 at [64,96))
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          umma_ts(tbase + C::kColDV, tbase + C::kColDP + (k < 4 ? k * 8 : 64 + (k - 4) * 8),
+                  umma_desc_sw128(doaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
+        umma_commit(dv_done);
         // dK += dS^T Q   (A = dS^T smem K-major, B = Q MN-major), q-halves committed separately
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          umma_ss(tbase + C::kColDK, umma_desc_sw128(dsaddr + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024),
+        for (int k = 0; k < 4; ++k)
+          umma_ss(tbase + C::kColDK, umma_desc_sw128(dsaddr + (k & 3) * 32, 16, 1024),
                   umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
-          if (k == 3) umma_commit(dka_done);
+        umma_commit(dka_done);
+        if (has_next) {
+          mbar_wait(dv_done, i & 1);  // P^T(i) consumed -> dP^T region free
+          tc_fence_after();
+          issue_dp(nstage);
         }
+#pragma unroll
+        for (int k = 4; k < 8; ++k)
+          umma_ss(tbase + C::kColDK, umma_desc_sw128(dsaddr + 16384 + (k & 3) * 32, 16, 1024),
+                  umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, 1u);
         umma_commit(dkb_done);
         umma_commit(&qd_empty[stage]);
         stage = nstage;
@@ -306,22 +315,17 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
       const float* sv = reinterpret_cast<const float*>(smem + C::kOffVec + stage * C::kVecBytes);
       mbar_wait(&qd_full[stage], phase);
       mbar_wait(s_full, i & 1);
-      mbar_wait(dp_full, i & 1);
       tc_fence_after();
+      // phase 1: P = exp2(S^T sl2 - lse2_q) for this warpgroup's 64 q columns
+      float pv[64];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int cb = wg * 64 + c * 32;
-        uint32_t sr[32], dr[32];
+        uint32_t sr[32];
         tmem_ld32(tbase + lane_off + C::kColS + cb, sr);
-        tmem_ld32(tbase + lane_off + C::kColDP + cb, dr);
         tmem_ld_wait();
-        float pv[32], ds[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float p = ex2_approx(fmaf(__uint_as_float(sr[j]), sl2, -sv[cb + j]));
-          pv[j] = p;
-          ds[j] = p * (__uint_as_float(dr[j]) - sv[128 + cb + j]);
-        }
+        for (int j = 0; j < 32; ++j) pv[32 * c + j] = ex2_approx(fmaf(__uint_as_float(sr[j]), sl2, -sv[cb + j]));
         if (need_mask) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -329,22 +333,39 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
             int lo, hi;
             row_interval(g, qseg, qrow, kseg, lo, hi);
             const bool vis = qrow < q1 && kpos < k1 && kpos >= lo && kpos < hi;
-            pv[j] = vis ? pv[j] : 0.f;
-            ds[j] = vis ? ds[j] : 0.f;
+            pv[32 * c + j] = vis ? pv[32 * c + j] : 0.f;
           }
+        }
+      }
+      // phase 2: dS = P (dP - D); P^T (bf16) over the dP^T columns just read
+      mbar_wait(dp_full, i & 1);
+      tc_fence_after();
+      uint32_t dsk[32];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int cb = wg * 64 + c * 32;
+        uint32_t dr[32];
+        tmem_ld32(tbase + lane_off + C::kColDP + cb, dr);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float d0 = pv[32 * c + 2 * j] * (__uint_as_float(dr[2 * j]) - sv[128 + cb + 2 * j]);
+          const float d1 = pv[32 * c + 2 * j + 1] * (__uint_as_float(dr[2 * j + 1]) - sv[128 + cb + 2 * j + 1]);
+          dsk[16 * c + j] = pack_bf16x2(d0, d1);
         }
         uint32_t pk[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(pv[2 * j], pv[2 * j + 1]);
-        tmem_st16(tbase + lane_off + C::kColS + wg * 64 + c * 16, pk);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(ds[2 * j], ds[2 * j + 1]);
-        if (c == 0 && i > 0) mbar_wait(my_dk_done, (i - 1) & 1);  // dK(i-1) has read this dS^T half
+        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(pv[32 * c + 2 * j], pv[32 * c + 2 * j + 1]);
+        tmem_st16(tbase + lane_off + C::kColDP + wg * 64 + c * 16, pk);
+      }
+      // dS^T (bf16) into smem, K-major rows = keys, block wg = q half
+      if (i > 0) mbar_wait(my_dk_done, (i - 1) & 1);  // dK(i-1) has read this dS^T half
+      {
         uint8_t* dsrow = sDS + wg * 16384;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          *reinterpret_cast<uint4*>(dsrow + sw128_offset(r, c * 4 + u)) =
-              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        for (int u = 0; u < 8; ++u)
+          *reinterpret_cast<uint4*>(dsrow + sw128_offset(r, u)) =
+              make_uint4(dsk[4 * u], dsk[4 * u + 1], dsk[4 * u + 2], dsk[4 * u + 3]);
       }
       tmem_st_wait();
       fence_proxy_async_smem();
@@ -521,6 +542,10 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         umma_commit(dp_full);
         umma_commit(&kv_empty[slot(2 * j + 1)]);  // V(j) consumed
       };
+      // Prologue S(0), dP(0), S(1); then per tile, after compute(j): dQ(j),
+      // dP(j+1) (dP region read by compute(j)), S(j+2) into the buffer dQ(j)
+      // has just consumed.  compute(j+1) phase 1 (exp of S(j+1)) overlaps
+      // dQ(j) and dP(j+1).
       mbar_wait(q_full, 0);
       mbar_wait(&kv_full[slot(0)], ph(0));
       tc_fence_after();
@@ -528,20 +553,14 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
       mbar_wait(&kv_full[slot(1)], ph(1));
       tc_fence_after();
       issue_dp(0);
+      if (n_kt > 1) {
+        mbar_wait(&kv_full[slot(2)], ph(2));
+        tc_fence_after();
+        issue_s(1);
+      }
       for (int j = 0; j < n_kt; ++j) {
-        if (j + 1 < n_kt) {
-          mbar_wait(&kv_full[slot(2 * j + 2)], ph(2 * j + 2));
-          if (j >= 1) mbar_wait(dq_done, (j - 1) & 1);  // dS(j-1) in S[(j+1)&1] consumed
-          tc_fence_after();
-          issue_s(j + 1);
-        }
         mbar_wait(compute_done, j & 1);
         tc_fence_after();
-        if (j + 1 < n_kt) {
-          mbar_wait(&kv_full[slot(2 * j + 3)], ph(2 * j + 3));
-          tc_fence_after();
-          issue_dp(j + 1);  // dP region was read by compute(j)
-        }
         // dQ += dS(j) K(j): A = dS bf16 in S[j&1] (keys 0..63 at +0, 64..127 at +64)
         const uint32_t sbase = tbase + ((j & 1) ? C::kColS1 : C::kColS0);
         const uint32_t kaddr = ring(2 * j);
@@ -551,6 +570,17 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
                   umma_desc_sw128(kaddr + k * 2048, 16384, 1024), idesc_q, (j > 0 || k > 0) ? 1u : 0u);
         umma_commit(dq_done);
         umma_commit(&kv_empty[slot(2 * j)]);  // K(j) consumed
+        if (j + 1 < n_kt) {
+          mbar_wait(&kv_full[slot(2 * j + 3)], ph(2 * j + 3));
+          tc_fence_after();
+          issue_dp(j + 1);
+        }
+        if (j + 2 < n_kt) {
+          mbar_wait(&kv_full[slot(2 * j + 4)], ph(2 * j + 4));
+          mbar_wait(dq_done, j & 1);  // dS(j) in S[j&1] consumed
+          tc_fence_after();
+          issue_s(j + 2);
+        }
       }
       umma_commit(acc_done);
     }
@@ -577,28 +607,36 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
       const int hi = min(xt ? hi1 : hi0, k1) - k0;
       const uint32_t sbase = tbase + lane_off + ((j & 1) ? C::kColS1 : C::kColS0);
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      // phase 1: P = exp2(S sl2 - lse2) for this warpgroup's 64 key columns
+      float pv[64];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int cb = wg * 64 + c * 32;
+        uint32_t sr[32];
+        tmem_ld32(sbase + cb, sr);
+        tmem_ld_wait();
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) pv[32 * c + jj] = ex2_approx(fmaf(__uint_as_float(sr[jj]), sl2, -lse2));
+        if (need_mask) {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) pv[32 * c + jj] = (cb + jj >= lo && cb + jj < hi) ? pv[32 * c + jj] : 0.f;
+        }
+      }
+      // phase 2: dS = P (dP - D) -> bf16 over the S columns already read
       mbar_wait(dp_full, j & 1);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int cb = wg * 64 + c * 32;
-        uint32_t sr[32], dr[32];
-        tmem_ld32(sbase + cb, sr);
+        uint32_t dr[32];
         tmem_ld32(tbase + lane_off + C::kColDP + cb, dr);
         tmem_ld_wait();
-        float ds[32];
-#pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
-          const float p = ex2_approx(fmaf(__uint_as_float(sr[jj]), sl2, -lse2));
-          ds[jj] = p * (__uint_as_float(dr[jj]) - dsum);
-        }
-        if (need_mask) {
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) ds[jj] = (cb + jj >= lo && cb + jj < hi) ? ds[jj] : 0.f;
-        }
         uint32_t pk[16];
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) pk[jj] = pack_bf16x2(ds[2 * jj], ds[2 * jj + 1]);
+        for (int jj = 0; jj < 16; ++jj)
+          pk[jj] = pack_bf16x2(pv[32 * c + 2 * jj] * (__uint_as_float(dr[2 * jj]) - dsum),
+                               pv[32 * c + 2 * jj + 1] * (__uint_as_float(dr[2 * jj + 1]) - dsum));
         tmem_st16(sbase + wg * 64 + c * 16, pk);
       }
       tmem_st_wait();
