@@ -33,6 +33,7 @@
 #include "attn_common.h"
 
 #include <cuda_bf16.h>
+#include <cstdlib>
 
 namespace bd {
 namespace {
@@ -78,6 +79,15 @@ __global__ void zero_kernel(float4* __restrict__ p, size_t n4) {
     p[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
+// Opt-in event trace (BD_TRACE=1 in the environment): one CTA records clock64
+// stamps of its pipeline hand-offs into a static device buffer, read back by
+// bd_debug_trace().  Off by default (a warp-uniform predicate per event).
+__device__ long long g_trace[8192];
+#define TRACE(slot, cond)                                         \
+  do {                                                            \
+    if (a.trace && (cond)) g_trace[(slot)] = clock64();           \
+  } while (0)
+
 struct BwdArgs {
   const int* map;
   const float* lse2_t;
@@ -88,6 +98,7 @@ struct BwdArgs {
   int batch, n_q_heads, n_kv_heads, group, N;
   Geom g;
   float scale, scale_log2;
+  int trace;  // 1 = record the trace for blockIdx.x == 0
 };
 
 __device__ __forceinline__ void store_row_bf16(__nv_bfloat16* dst, const uint32_t* v, float mul, bool ok) {
@@ -101,29 +112,54 @@ __device__ __forceinline__ void store_row_bf16(__nv_bfloat16* dst, const uint32_
   }
 }
 
+template <int N>
+__device__ __forceinline__ void store_row_bf16_n(__nv_bfloat16* dst, const uint32_t* v, float mul, bool ok) {
+  uint32_t pk[N / 2];
+#pragma unroll
+  for (int j = 0; j < N / 2; ++j) pk[j] = pack_bf16x2(__uint_as_float(v[2 * j]) * mul, __uint_as_float(v[2 * j + 1]) * mul);
+  if (ok) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int u = 0; u < N / 8; ++u) d4[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+  }
+}
+
 // ================================================================== dK/dV
+// Smem: K, V resident; Q(i), dO(i) through a 4-slot single-tile ring (Q(i) ->
+// ring index 2i, dO(i) -> 2i+1, each released by its last MMA); dS^T (bf16)
+// in smem; LSE/D vectors through a 2-slot ring.  TMEM: S^T [0,128),
+// dP^T [128,256), dV, dK.  Four compute warpgroups each own 32 q columns
+// (a thread = one key row = one TMEM lane).  Per iteration i:
+//   phase 1 (needs S^T(i)):  P = exp2(S sl2 - lse2)          -> p1_done
+//   phase 2 (needs dP^T(i)): dS = P (dP - D); P^T (bf16) over the dP^T
+//            columns just read -> pt_done; dS^T to smem      -> ds_done
+//   MMA: S^T(i+1) at p1_done(i); dV(i) at pt_done(i); dK(i) at ds_done(i);
+//        dP^T(i+1) once dV(i) has consumed P^T(i).
+// (dK(i) before dP^T(i+1) so that storing dS^T(i+1) never waits for dK(i).)
 template <int D>
 struct DkdvCfg {
   static constexpr int kTileBytes = 128 * D * 2;
-  static constexpr int kStages = 2;
-  static constexpr int kComputeWarps = 8;
-  static constexpr int kTmaWarp = 8;
-  static constexpr int kMmaWarp = 9;
-  static constexpr int kThreads = 320;
+  static constexpr int kSlots = 4;
+  static constexpr int kWGs = 4;
+  static constexpr int kCols = 128 / kWGs;  // q columns per warpgroup
+  static constexpr int kComputeWarps = 4 * kWGs;
+  static constexpr int kTmaWarp = kComputeWarps;
+  static constexpr int kMmaWarp = kComputeWarps + 1;
+  static constexpr int kThreads = 32 * (kComputeWarps + 2);
   static constexpr int kColS = 0, kColDP = 128, kColDV = 256, kColDK = 256 + D;
   static constexpr uint32_t kTmemCols = 512;
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kTileBytes;
   static constexpr int kOffDS = 2 * kTileBytes;
-  static constexpr int kDsBytes = 128 * 128 * 2;
-  static constexpr int kOffStage = kOffDS + kDsBytes;
-  static constexpr int kStageBytes = 2 * kTileBytes;
-  static constexpr int kOffVec = kOffStage + kStages * kStageBytes;
+  static constexpr int kOffRing = kOffDS + 128 * 128 * 2;
+  static constexpr int kOffVec = kOffRing + kSlots * kTileBytes;
   static constexpr int kVecBytes = 2 * 128 * 4;
-  static constexpr int kOffBar = kOffVec + kStages * kVecBytes;
-  // kv_full, qd_full[2], qd_empty[2], s_full, dp_full, compute_done, dv_done, dka_done, dkb_done, acc_done
-  static constexpr int kNumBars = 1 + 2 * kStages + 8;
+  static constexpr int kOffBar = kOffVec + 2 * kVecBytes;
+  // kv_full, slot_full[S], slot_empty[S], vec_full[2], vec_empty[2], s_full, dp_full, p1_done, pt_done,
+  // ds_done, dv_done, dk_done, acc_done
+  static constexpr int kNumBars = 1 + 2 * kSlots + 4 + 8;
   static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16;
+  static_assert(kSmemBytes <= 232448, "dkdv smem budget");
 };
 
 template <int D>
@@ -136,17 +172,21 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
   uint8_t* sK = smem + C::kOffK;
   uint8_t* sV = smem + C::kOffV;
   uint8_t* sDS = smem + C::kOffDS;
+  uint8_t* sRing = smem + C::kOffRing;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* kv_full = bars;
-  uint64_t* qd_full = bars + 1;
-  uint64_t* qd_empty = qd_full + C::kStages;
-  uint64_t* s_full = qd_empty + C::kStages;
+  uint64_t* slot_full = bars + 1;
+  uint64_t* slot_empty = slot_full + C::kSlots;
+  uint64_t* vec_full = slot_empty + C::kSlots;  // [2]
+  uint64_t* vec_empty = vec_full + 2;           // [2]
+  uint64_t* s_full = vec_empty + 2;
   uint64_t* dp_full = s_full + 1;
-  uint64_t* compute_done = dp_full + 1;
-  uint64_t* dv_done = compute_done + 1;
-  uint64_t* dka_done = dv_done + 1;
-  uint64_t* dkb_done = dka_done + 1;
-  uint64_t* acc_done = dkb_done + 1;
+  uint64_t* p1_done = dp_full + 1;  // S^T(i) read
+  uint64_t* pt_done = p1_done + 1;  // dP^T(i) read, P^T(i) written over it
+  uint64_t* ds_done = pt_done + 1;  // dS^T(i) in smem
+  uint64_t* dv_done = ds_done + 1;
+  uint64_t* dk_done = dv_done + 1;
+  uint64_t* acc_done = dk_done + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
@@ -165,20 +205,27 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
   const int* ents = mv.col_ent() + e0;
   const int n_it = n_qt * a.group;
   const int k0 = tile_start(g, kt), k1 = tile_end(g, kt), kseg = tile_seg(g, kt);
+  auto slot_of = [](int idx) { return idx % C::kSlots; };
+  auto phase_of = [](int idx) { return (uint32_t)((idx / C::kSlots) & 1); };
 
   if (warp == 0) tmem_alloc<C::kTmemCols>(tslot);
   if (warp == C::kTmaWarp && lane == 0) {
     mbar_init(kv_full, 1);
-    for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&qd_full[s], 1);
-      mbar_init(&qd_empty[s], 1);
+    for (int s = 0; s < C::kSlots; ++s) {
+      mbar_init(&slot_full[s], 1);
+      mbar_init(&slot_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&vec_full[s], 1);
+      mbar_init(&vec_empty[s], C::kComputeWarps);
     }
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
-    mbar_init(compute_done, C::kComputeWarps);
+    mbar_init(p1_done, C::kComputeWarps);
+    mbar_init(pt_done, C::kComputeWarps);
+    mbar_init(ds_done, C::kComputeWarps);
     mbar_init(dv_done, 1);
-    mbar_init(dka_done, 1);
-    mbar_init(dkb_done, 1);
+    mbar_init(dk_done, 1);
     mbar_init(acc_done, 1);
     fence_barrier_init();
   }
@@ -195,27 +242,26 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
         tma_load_4d(sK + kb * 16384, &tmK, kv_full, kb * 64, kvh, k0, b);
         tma_load_4d(sV + kb * 16384, &tmV, kv_full, kb * 64, kvh, k0, b);
       }
-      int stage = 0;
-      uint32_t phase = 0;
       for (int i = 0; i < n_it; ++i) {
-        const int qt = entry_tile(ents[i / a.group]);
+        const int qt = entry_tile(ents[n_qt - 1 - i / a.group]);  // decreasing q-tile: L2 reuse across CTAs
         const int h = kvh * a.group + (i % a.group);
         const int q0 = tile_start(g, qt);
-        mbar_wait(&qd_empty[stage], phase ^ 1);
-        mbar_expect_tx(&qd_full[stage], 2 * C::kTileBytes + C::kVecBytes);
-        uint8_t* sq = smem + C::kOffStage + stage * C::kStageBytes;
-        for (int kb = 0; kb < D / 64; ++kb) {
-          tma_load_4d(sq + kb * 16384, &tmQ, &qd_full[stage], kb * 64, h, q0, b);
-          tma_load_4d(sq + C::kTileBytes + kb * 16384, &tmDO, &qd_full[stage], kb * 64, h, q0, b);
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {  // w = 0: Q(i), w = 1: dO(i)
+          const int idx = 2 * i + w, s = slot_of(idx);
+          mbar_wait(&slot_empty[s], phase_of(idx) ^ 1);
+          TRACE(2048 + 8 * (i & 127) + w, blockIdx.x == 0);
+          mbar_expect_tx(&slot_full[s], C::kTileBytes);
+          for (int kb = 0; kb < D / 64; ++kb)
+            tma_load_4d(sRing + s * C::kTileBytes + kb * 16384, w ? &tmDO : &tmQ, &slot_full[s], kb * 64, h, q0, b);
         }
+        const int vs = i & 1;
+        mbar_wait(&vec_empty[vs], ((i >> 1) & 1) ^ 1);
+        mbar_expect_tx(&vec_full[vs], C::kVecBytes);
         const size_t vec = (((size_t)b * a.n_q_heads + h) * g.NT + qt) * kTileRows;
-        float* sv = reinterpret_cast<float*>(smem + C::kOffVec + stage * C::kVecBytes);
-        bulk_load(sv, a.lse2_t + vec, 512, &qd_full[stage]);
-        bulk_load(sv + 128, a.dsum_t + vec, 512, &qd_full[stage]);
-        if (++stage == C::kStages) {
-          stage = 0;
-          phase ^= 1;
-        }
+        float* sv = reinterpret_cast<float*>(smem + C::kOffVec + vs * C::kVecBytes);
+        bulk_load(sv, a.lse2_t + vec, 512, &vec_full[vs]);
+        bulk_load(sv + 128, a.dsum_t + vec, 512, &vec_full[vs]);
       }
     }
   } else if (warp == C::kMmaWarp) {
@@ -224,9 +270,9 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);  // S^T, dP^T
       constexpr uint32_t idesc_kv = umma_idesc_bf16(128, D, false, true);    // dV, dK: B MN-major
       const uint32_t kaddr = smem_u32(sK), vaddr = smem_u32(sV), dsaddr = smem_u32(sDS);
-      auto stage_addr = [&](int st) { return smem_u32(smem + C::kOffStage + st * C::kStageBytes); };
-      auto issue_s = [&](int st) {  // S^T = K Q^T
-        const uint32_t qaddr = stage_addr(st);
+      auto ring = [&](int idx) { return smem_u32(sRing + slot_of(idx) * C::kTileBytes); };
+      auto issue_s = [&](int i) {  // S^T = K Q^T
+        const uint32_t qaddr = ring(2 * i);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
@@ -235,8 +281,8 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
         }
         umma_commit(s_full);
       };
-      auto issue_dp = [&](int st) {  // dP^T = V dO^T
-        const uint32_t doaddr = stage_addr(st) + C::kTileBytes;
+      auto issue_dp = [&](int i) {  // dP^T = V dO^T
+        const uint32_t doaddr = ring(2 * i + 1);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
@@ -246,160 +292,163 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
         umma_commit(dp_full);
       };
       mbar_wait(kv_full, 0);
-      mbar_wait(&qd_full[0], 0);
+      mbar_wait(&slot_full[slot_of(0)], phase_of(0));
       tc_fence_after();
       issue_s(0);
+      mbar_wait(&slot_full[slot_of(1)], phase_of(1));
+      tc_fence_after();
       issue_dp(0);
-      int stage = 0;
-      uint32_t phase = 0;
-      // Per iteration, after compute(i): S^T(i+1) (S region is free: compute(i)
-      // read it in phase 1), dV(i) (P^T(i) lives in the dP region), dK(i) first
-      // q-half, dP^T(i+1) once dV(i) has consumed P^T(i), dK(i) second half.
-      // compute(i+1) phase 1 (exp) overlaps dV/dK; phase 2 needs dP^T(i+1).
       for (int i = 0; i < n_it; ++i) {
-        const uint32_t qaddr = stage_addr(stage);
-        const uint32_t doaddr = qaddr + C::kTileBytes;
-        const int nstage = stage + 1 == C::kStages ? 0 : stage + 1;
-        const uint32_t nphase = stage + 1 == C::kStages ? phase ^ 1 : phase;
         const bool has_next = i + 1 < n_it;
-        mbar_wait(compute_done, i & 1);
-        tc_fence_after();
+        const uint32_t qaddr = ring(2 * i), doaddr = ring(2 * i + 1);
+        mbar_wait(p1_done, i & 1);
+        TRACE(1024 + 8 * (i & 127) + 0, blockIdx.x == 0);
         if (has_next) {
-          mbar_wait(&qd_full[nstage], nphase);
+          mbar_wait(&slot_full[slot_of(2 * i + 2)], phase_of(2 * i + 2));
+          TRACE(1024 + 8 * (i & 127) + 6, blockIdx.x == 0);
           tc_fence_after();
-          issue_s(nstage);
+          issue_s(i + 1);
         }
-        // dV += P^T dO   (A = P^T in TMEM: q 0..63 at dP cols [0,32), q 64..127 at [64,96))
+        mbar_wait(pt_done, i & 1);
+        TRACE(1024 + 8 * (i & 127) + 1, blockIdx.x == 0);
+        tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          umma_ts(tbase + C::kColDV, tbase + C::kColDP + (k < 4 ? k * 8 : 64 + (k - 4) * 8),
+        for (int k = 0; k < 8; ++k)  // dV += P^T dO; P^T of q block k at dP cols 32(k/2) + 8(k%2)
+          umma_ts(tbase + C::kColDV, tbase + C::kColDP + 32 * (k >> 1) + 8 * (k & 1),
                   umma_desc_sw128(doaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
         umma_commit(dv_done);
-        // dK += dS^T Q   (A = dS^T smem K-major, B = Q MN-major), q-halves committed separately
+        umma_commit(&slot_empty[slot_of(2 * i + 1)]);  // dO(i) consumed
+        mbar_wait(ds_done, i & 1);
+        TRACE(1024 + 8 * (i & 127) + 3, blockIdx.x == 0);
+        tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          umma_ss(tbase + C::kColDK, umma_desc_sw128(dsaddr + (k & 3) * 32, 16, 1024),
+        for (int k = 0; k < 8; ++k)  // dK += dS^T Q (A = dS^T smem K-major, B = Q MN-major)
+          umma_ss(tbase + C::kColDK, umma_desc_sw128(dsaddr + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024),
                   umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
-        umma_commit(dka_done);
+        TRACE(1024 + 8 * (i & 127) + 5, blockIdx.x == 0);
+        umma_commit(dk_done);
+        umma_commit(&slot_empty[slot_of(2 * i)]);  // Q(i) consumed
         if (has_next) {
-          mbar_wait(dv_done, i & 1);  // P^T(i) consumed -> dP^T region free
+          mbar_wait(&slot_full[slot_of(2 * i + 3)], phase_of(2 * i + 3));
+          TRACE(1024 + 8 * (i & 127) + 4, blockIdx.x == 0);
+          mbar_wait(dv_done, i & 1);  // P^T(i) consumed -> dP^T columns free
+          TRACE(1024 + 8 * (i & 127) + 2, blockIdx.x == 0);
           tc_fence_after();
-          issue_dp(nstage);
+          issue_dp(i + 1);
         }
-#pragma unroll
-        for (int k = 4; k < 8; ++k)
-          umma_ss(tbase + C::kColDK, umma_desc_sw128(dsaddr + 16384 + (k & 3) * 32, 16, 1024),
-                  umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, 1u);
-        umma_commit(dkb_done);
-        umma_commit(&qd_empty[stage]);
-        stage = nstage;
-        phase = nphase;
       }
       umma_commit(acc_done);
     }
   } else {
     // ========================================================== compute
-    const int wg = warp >> 2;                 // q-column half
+    constexpr int NC = C::kCols;
+    const int wg = warp >> 2;                 // q columns [NC wg, NC wg + NC)
     const int r = (warp & 3) * 32 + lane;     // key row within the tile == TMEM lane
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const float sl2 = a.scale_log2;
     const int kpos = k0 + r;
-    uint64_t* my_dk_done = wg ? dkb_done : dka_done;
-    int stage = 0;
-    uint32_t phase = 0;
+    const uint32_t tS = tbase + lane_off + C::kColS + wg * NC;
+    const uint32_t tP = tbase + lane_off + C::kColDP + wg * NC;
     for (int i = 0; i < n_it; ++i) {
-      const int ent = ents[i / a.group];
+      const int ent = ents[n_qt - 1 - i / a.group];
       const int qt = entry_tile(ent);
       const int q0 = tile_start(g, qt), q1 = tile_end(g, qt), qseg = tile_seg(g, qt);
       const bool need_mask = entry_kind(ent) == kKindPartial || (q1 - q0) < 128 || (k1 - k0) < 128;
-      const float* sv = reinterpret_cast<const float*>(smem + C::kOffVec + stage * C::kVecBytes);
-      mbar_wait(&qd_full[stage], phase);
+      const float* sv = reinterpret_cast<const float*>(smem + C::kOffVec + (i & 1) * C::kVecBytes) + wg * NC;
+      mbar_wait(&vec_full[i & 1], (i >> 1) & 1);
+      TRACE(8 * (i & 127) + 0, blockIdx.x == 0 && threadIdx.x == 0);
       mbar_wait(s_full, i & 1);
+      TRACE(8 * (i & 127) + 1, blockIdx.x == 0 && threadIdx.x == 0);
       tc_fence_after();
-      // phase 1: P = exp2(S^T sl2 - lse2_q) for this warpgroup's 64 q columns
-      float pv[64];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int cb = wg * 64 + c * 32;
-        uint32_t sr[32];
-        tmem_ld32(tbase + lane_off + C::kColS + cb, sr);
+      // phase 1: P = exp2(S^T sl2 - lse2_q)
+      float pv[NC];
+      {
+        uint32_t sr[NC];
+        tmem_ld32(tS, sr);
         tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p1_done);  // S^T(i) read: S^T(i+1) may be issued
 #pragma unroll
-        for (int j = 0; j < 32; ++j) pv[32 * c + j] = ex2_approx(fmaf(__uint_as_float(sr[j]), sl2, -sv[cb + j]));
+        for (int j = 0; j < NC; ++j) pv[j] = ex2_approx(fmaf(__uint_as_float(sr[j]), sl2, -sv[j]));
         if (need_mask) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int qrow = q0 + cb + j;
+          for (int j = 0; j < NC; ++j) {
+            const int qrow = q0 + wg * NC + j;
             int lo, hi;
             row_interval(g, qseg, qrow, kseg, lo, hi);
             const bool vis = qrow < q1 && kpos < k1 && kpos >= lo && kpos < hi;
-            pv[32 * c + j] = vis ? pv[32 * c + j] : 0.f;
+            pv[j] = vis ? pv[j] : 0.f;
           }
         }
       }
+      TRACE(8 * (i & 127) + 2, blockIdx.x == 0 && threadIdx.x == 0);
       // phase 2: dS = P (dP - D); P^T (bf16) over the dP^T columns just read
       mbar_wait(dp_full, i & 1);
+      TRACE(8 * (i & 127) + 3, blockIdx.x == 0 && threadIdx.x == 0);
       tc_fence_after();
-      uint32_t dsk[32];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int cb = wg * 64 + c * 32;
-        uint32_t dr[32];
-        tmem_ld32(tbase + lane_off + C::kColDP + cb, dr);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float d0 = pv[32 * c + 2 * j] * (__uint_as_float(dr[2 * j]) - sv[128 + cb + 2 * j]);
-          const float d1 = pv[32 * c + 2 * j + 1] * (__uint_as_float(dr[2 * j + 1]) - sv[128 + cb + 2 * j + 1]);
-          dsk[16 * c + j] = pack_bf16x2(d0, d1);
-        }
-        uint32_t pk[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(pv[32 * c + 2 * j], pv[32 * c + 2 * j + 1]);
-        tmem_st16(tbase + lane_off + C::kColDP + wg * 64 + c * 16, pk);
-      }
-      // dS^T (bf16) into smem, K-major rows = keys, block wg = q half
-      if (i > 0) mbar_wait(my_dk_done, (i - 1) & 1);  // dK(i-1) has read this dS^T half
+      uint32_t dsk[NC / 2];
       {
-        uint8_t* dsrow = sDS + wg * 16384;
+        uint32_t dr[NC];
+        tmem_ld32(tP, dr);
+        tmem_ld_wait();
+        uint32_t pk[NC / 2];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          *reinterpret_cast<uint4*>(dsrow + sw128_offset(r, u)) =
-              make_uint4(dsk[4 * u], dsk[4 * u + 1], dsk[4 * u + 2], dsk[4 * u + 3]);
+        for (int j = 0; j < NC / 2; ++j) {
+          const float p0 = pv[2 * j], p1 = pv[2 * j + 1];
+          dsk[j] = pack_bf16x2(p0 * (__uint_as_float(dr[2 * j]) - sv[128 + 2 * j]),
+                               p1 * (__uint_as_float(dr[2 * j + 1]) - sv[128 + 2 * j + 1]));
+          pk[j] = pack_bf16x2(p0, p1);
+        }
+        tmem_st16(tP, pk);
       }
       tmem_st_wait();
-      fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(compute_done);
-      if (++stage == C::kStages) {
-        stage = 0;
-        phase ^= 1;
+      if (lane == 0) {
+        mbar_arrive(pt_done);
+        mbar_arrive(&vec_empty[i & 1]);
       }
+      // dS^T (bf16) into smem: K-major rows = keys; q columns [NC wg, +NC) are
+      // block (wg / 2), 16-byte chunks 4 (wg % 2) .. +3
+      if (i > 0) mbar_wait(dk_done, (i - 1) & 1);  // dK(i-1) has read dS^T(i-1)
+      {
+        uint8_t* dsrow = sDS + (wg >> 1) * 16384;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          *reinterpret_cast<uint4*>(dsrow + sw128_offset(r, (wg & 1) * 4 + u)) =
+              make_uint4(dsk[4 * u], dsk[4 * u + 1], dsk[4 * u + 2], dsk[4 * u + 3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_done);
+      TRACE(8 * (i & 127) + 4, blockIdx.x == 0 && threadIdx.x == 0);
     }
-    // ---- epilogue: dK (scaled), dV -> bf16
+    // ---- epilogue: dK (scaled), dV -> bf16; warpgroup wg stores columns [D/4 wg, +D/4)
     if (n_it > 0) {
       mbar_wait(acc_done, 0);
       tc_fence_after();
     }
     const bool ok = kpos < k1;
-    const size_t orow = (((size_t)b * a.N + kpos) * a.n_kv_heads + kvh) * D + wg * (D / 2);
+    constexpr int DC = D / C::kWGs;  // 32 (D = 128) or 16 (D = 64)
+    const size_t orow = (((size_t)b * a.N + kpos) * a.n_kv_heads + kvh) * D + wg * DC;
 #pragma unroll
     for (int which = 0; which < 2; ++which) {
-      const uint32_t col = (which ? C::kColDK : C::kColDV) + wg * (D / 2);
+      const uint32_t col = (which ? C::kColDK : C::kColDV) + wg * DC;
       const float mul = n_it > 0 ? (which ? a.scale : 1.f) : 0.f;
       __nv_bfloat16* out = (which ? a.dk : a.dv) + orow;
-#pragma unroll
-      for (int c = 0; c < D / 64; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tbase + lane_off + col + 32 * c, v);
-        tmem_ld_wait();
-        if (n_it == 0) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = 0u;
-        }
-        store_row_bf16(out + 32 * c, v, mul, ok);
+      uint32_t v[32];
+      if (DC == 32) {
+        tmem_ld32(tbase + lane_off + col, v);
+      } else {
+        tmem_ld16(tbase + lane_off + col, v);
       }
+      tmem_ld_wait();
+      if (n_it == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0u;
+      }
+      store_row_bf16_n<DC>(out, v, mul, ok);
     }
   }
   tc_fence_before();
@@ -422,8 +471,8 @@ struct DqCfg {
   static constexpr int kOffDO = kTileBytes;
   static constexpr int kOffRing = 2 * kTileBytes;
   static constexpr int kOffBar = kOffRing + kStages * kTileBytes;
-  // q_full, kv_full[S], kv_empty[S], s_full[2], dp_full, compute_done, dq_done, acc_done
-  static constexpr int kNumBars = 1 + 2 * kStages + 6;
+  // q_full, kv_full[S], kv_empty[S], s_full[2], dp_full, dp_free, compute_done, dq_done, acc_done
+  static constexpr int kNumBars = 1 + 2 * kStages + 7;
   static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16;
 };
 
@@ -443,7 +492,8 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
   uint64_t* kv_empty = kv_full + C::kStages;
   uint64_t* s_full = kv_empty + C::kStages;  // [2]
   uint64_t* dp_full = s_full + 2;
-  uint64_t* compute_done = dp_full + 1;
+  uint64_t* dp_free = dp_full + 1;       // compute has read dP(j)
+  uint64_t* compute_done = dp_free + 1;  // dS(j) written over S[j&1]
   uint64_t* dq_done = compute_done + 1;
   uint64_t* acc_done = dq_done + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
@@ -475,6 +525,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
     mbar_init(&s_full[0], 1);
     mbar_init(&s_full[1], 1);
     mbar_init(dp_full, 1);
+    mbar_init(dp_free, C::kComputeWarps);
     mbar_init(compute_done, C::kComputeWarps);
     mbar_init(dq_done, 1);
     mbar_init(acc_done, 1);
@@ -559,6 +610,12 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         issue_s(1);
       }
       for (int j = 0; j < n_kt; ++j) {
+        mbar_wait(dp_free, j & 1);
+        if (j + 1 < n_kt) {
+          mbar_wait(&kv_full[slot(2 * j + 3)], ph(2 * j + 3));
+          tc_fence_after();
+          issue_dp(j + 1);
+        }
         mbar_wait(compute_done, j & 1);
         tc_fence_after();
         // dQ += dS(j) K(j): A = dS bf16 in S[j&1] (keys 0..63 at +0, 64..127 at +64)
@@ -570,11 +627,6 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
                   umma_desc_sw128(kaddr + k * 2048, 16384, 1024), idesc_q, (j > 0 || k > 0) ? 1u : 0u);
         umma_commit(dq_done);
         umma_commit(&kv_empty[slot(2 * j)]);  // K(j) consumed
-        if (j + 1 < n_kt) {
-          mbar_wait(&kv_full[slot(2 * j + 3)], ph(2 * j + 3));
-          tc_fence_after();
-          issue_dp(j + 1);
-        }
         if (j + 2 < n_kt) {
           mbar_wait(&kv_full[slot(2 * j + 4)], ph(2 * j + 4));
           mbar_wait(dq_done, j & 1);  // dS(j) in S[j&1] consumed
@@ -626,19 +678,25 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
       // phase 2: dS = P (dP - D) -> bf16 over the S columns already read
       mbar_wait(dp_full, j & 1);
       tc_fence_after();
+      uint32_t pk[32];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int cb = wg * 64 + c * 32;
         uint32_t dr[32];
         tmem_ld32(tbase + lane_off + C::kColDP + cb, dr);
         tmem_ld_wait();
-        uint32_t pk[16];
+        if (c == 1) {  // dP(j) fully read: the MMA warp may overwrite it with dP(j+1)
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dp_free);
+        }
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj)
-          pk[jj] = pack_bf16x2(pv[32 * c + 2 * jj] * (__uint_as_float(dr[2 * jj]) - dsum),
-                               pv[32 * c + 2 * jj + 1] * (__uint_as_float(dr[2 * jj + 1]) - dsum));
-        tmem_st16(sbase + wg * 64 + c * 16, pk);
+          pk[16 * c + jj] = pack_bf16x2(pv[32 * c + 2 * jj] * (__uint_as_float(dr[2 * jj]) - dsum),
+                                        pv[32 * c + 2 * jj + 1] * (__uint_as_float(dr[2 * jj + 1]) - dsum));
       }
+      tmem_st16(sbase + wg * 64, pk);
+      tmem_st16(sbase + wg * 64 + 16, pk + 16);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -710,6 +768,8 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   a.g = g;
   a.scale = scale_of(p);
   a.scale_log2 = a.scale * kLog2e;
+  static const bool trace_on = getenv("BD_TRACE") != nullptr;
+  a.trace = trace_on ? 1 : 0;
   // 2. dK, dV
   const long long grid_kv = (long long)g.NT * p.batch * p.n_kv_heads;
   attn_bwd_dkdv_kernel<D><<<(unsigned)grid_kv, DkdvCfg<D>::kThreads, DkdvCfg<D>::kSmemBytes, stream>>>(
@@ -739,3 +799,8 @@ int run_attn_bwd(const bd_problem& p, const Geom& g, const void* q, const void* 
 }
 
 }  // namespace bd
+
+extern "C" int bd_debug_trace(int64_t* host_out, int n) {
+  if (!host_out || n <= 0 || n > 8192) return BD_ERR_INVALID_ARG;
+  return bd::check_cuda(cudaMemcpyFromSymbol(host_out, bd::g_trace, n * sizeof(long long)), "trace copy");
+}

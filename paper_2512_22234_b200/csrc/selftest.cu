@@ -164,3 +164,63 @@ extern "C" int bd_selftest_mma(const void* a, const void* b, const void* v, floa
   note_launches(1);
   return cudaGetLastError() == cudaSuccess ? BD_OK : BD_ERR_CUDA;
 }
+
+// ---------------------------------------------------------------------------
+// Diagnostic: TMA ingest bandwidth.  Every CTA streams 32 KB tiles (two
+// 64x128 bf16 boxes of a [rows, 128] tensor, 4-D map like the attention
+// operands: row stride `row_stride_elems`) through `stages` smem slots;
+// cycles[blockIdx] = clock64 span, bytes per CTA = iters * 32 KB.
+namespace bd {
+namespace {
+__global__ void __launch_bounds__(64, 1)
+    tma_bw_kernel(const __grid_constant__ CUtensorMap tm, int n_tiles, int iters, int stages, long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 6 * 32768);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const long long t0 = clock64();
+    const int start = (blockIdx.x * 7) % n_tiles;
+    for (int s = 0; s < stages && s < iters; ++s) {
+      mbar_expect_tx(&full[s], 32768);
+      const int t = (start + s) % n_tiles;
+      tma_load_4d(smem + s * 32768, &tm, &full[s], 0, 0, t * 128, 0);
+      tma_load_4d(smem + s * 32768 + 16384, &tm, &full[s], 64, 0, t * 128, 0);
+    }
+    for (int i = 0; i < iters; ++i) {
+      const int s = i % stages;
+      mbar_wait(&full[s], (i / stages) & 1);
+      const int nx = i + stages;
+      if (nx < iters) {
+        mbar_expect_tx(&full[s], 32768);
+        const int t = (start + nx) % n_tiles;
+        tma_load_4d(smem + s * 32768, &tm, &full[s], 0, 0, t * 128, 0);
+        tma_load_4d(smem + s * 32768 + 16384, &tm, &full[s], 64, 0, t * 128, 0);
+      }
+    }
+    cycles[blockIdx.x] = clock64() - t0;
+  }
+}
+}  // namespace
+}  // namespace bd
+
+extern "C" int bd_bench_tma(const void* src, int64_t rows, int heads, int grid, int iters, int stages,
+                            long long* cycles, void* stream_) {
+  using namespace bd;
+  CUtensorMap tm;
+  // [rows, heads, 128] bf16 viewed as dims (128, heads, rows, 1), box (64, 1, 128, 1)
+  const uint64_t dims[4] = {128, (uint64_t)heads, (uint64_t)rows, 1};
+  const uint64_t strides[3] = {256, (uint64_t)heads * 256, (uint64_t)rows * heads * 256};
+  const uint32_t box[4] = {64, 1, 128, 1};
+  if (!make_tmap_bf16(&tm, src, 4, dims, strides, box)) return BD_ERR_CUDA;
+  if (stages < 1 || stages > 6) return BD_ERR_INVALID_ARG;
+  const int smem = 6 * 32768 + 64 + 1024;
+  cudaFuncSetAttribute(tma_bw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  tma_bw_kernel<<<grid, 64, smem, static_cast<cudaStream_t>(stream_)>>>(tm, (int)(rows / 128), iters, stages,
+                                                                          cycles);
+  return cudaGetLastError() == cudaSuccess ? BD_OK : BD_ERR_CUDA;
+}
