@@ -79,8 +79,8 @@ int64_t bd_packed_len(const bd_problem* prob);
 
 /* Workspace bytes needed by bd_attn_fwd (backward = 0) or bd_attn_bwd
  * (backward = 1).  The forward workspace holds the tile map; the backward
- * one additionally holds D = rowsum(dO * O) [b, Hq, Ntot] fp32 and the fp32
- * dQ accumulator [b, Ntot, Hq, d].  Returns 0 for an invalid problem. */
+ * one additionally holds D = rowsum(dO * O) and the log2-scaled LSE, fp32,
+ * tile-major [b, Hq, n_tiles, 128].  Returns 0 for an invalid problem. */
 size_t bd_attn_workspace_bytes(const bd_problem* prob, int backward);
 
 /* Forward.
@@ -98,8 +98,9 @@ int bd_attn_fwd(const bd_problem* prob, const void* q, const void* k, const void
 /* Backward of bd_attn_fwd for upstream gradient dout (bf16, like q), given the
  * forward's o and lse.  Writes dq (bf16 like q) and dk, dv (bf16 like k); dk
  * and dv sum over the Hq/Hkv query heads of each kv head.  ws must be
- * >= bd_attn_workspace_bytes(prob, 1) bytes.  The dQ reduction order is not
- * deterministic (fp32 atomics). */
+ * >= bd_attn_workspace_bytes(prob, 1) bytes.  Three kernels (preprocess,
+ * dK/dV over the column tile map, dQ over the row tile map); no atomics, so
+ * the result is deterministic. */
 int bd_attn_bwd(const bd_problem* prob, const void* q, const void* k, const void* v, const void* o,
                 const float* lse, const void* dout, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
                 void* stream);
@@ -161,6 +162,12 @@ int bd_tilemap_dump(const bd_problem* prob, int32_t* host_out, size_t cap, int64
 /* Tile-map statistics (host): counts of q-tiles, non-empty, FULL and PARTIAL
  * tiles per (sequence, head); out = int64[4]. */
 int bd_tilemap_stats(const bd_problem* prob, int64_t* out);
+
+/* Diagnostic (host): checks that the per-row visible-key intervals used by the
+ * forward/dQ kernels and the per-key visible-row intervals used by the dK/dV
+ * kernel describe the same mask for every (row, key); *mismatches (host)
+ * receives the count (0 expected).  Small problems only (Ntot^2 <= 2^26). */
+int bd_tilemap_selfcheck(const bd_problem* prob, int64_t* mismatches);
 
 const char* bd_error_string(int code);
 const char* bd_last_error(void);

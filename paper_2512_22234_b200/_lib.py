@@ -47,6 +47,7 @@ SIGNATURES = {
     "bd_dipo_token_loss": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P, _I32, _F, _P, _P, _P]),
     "bd_tilemap_dump": (ctypes.c_int, [_PROB, ctypes.POINTER(_I32), _SZ, ctypes.POINTER(_I64)]),
     "bd_tilemap_stats": (ctypes.c_int, [_PROB, ctypes.POINTER(_I64)]),
+    "bd_tilemap_selfcheck": (ctypes.c_int, [_PROB, ctypes.POINTER(_I64)]),
     "bd_error_string": (ctypes.c_char_p, [ctypes.c_int]),
     "bd_last_error": (ctypes.c_char_p, []),
     "bd_selftest_mma": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),

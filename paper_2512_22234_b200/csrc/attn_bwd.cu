@@ -124,6 +124,29 @@ __device__ __forceinline__ void store_row_bf16_n(__nv_bfloat16* dst, const uint3
   }
 }
 
+// P = 2^(s sl2 - lse2) for NC columns, zeroed outside [ja, jb) when MASKED
+// (dK/dV kernel: per-column lse2 from smem).  Masked and unmasked tiles take
+// separate code paths so FULL tiles pay no per-element mask work.
+template <bool MASKED, int NC>
+__device__ __forceinline__ void p_tile(const uint32_t* sr, const float* sv, float sl2, int ja, int jb, float* pv) {
+#pragma unroll
+  for (int j = 0; j < NC; ++j) pv[j] = ex2_mix(j, fmaf(__uint_as_float(sr[j]), sl2, -sv[j]));
+  if (MASKED) {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) pv[j] = (j >= ja && j < jb) ? pv[j] : 0.f;
+  }
+}
+// Same with a per-row lse2 (dQ kernel), 32 columns.
+template <bool MASKED>
+__device__ __forceinline__ void p_row(const uint32_t* sr, float lse2, float sl2, int ja, int jb, float* pv) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) pv[j] = ex2_mix(j, fmaf(__uint_as_float(sr[j]), sl2, -lse2));
+  if (MASKED) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) pv[j] = (j >= ja && j < jb) ? pv[j] : 0.f;
+  }
+}
+
 // ================================================================== dK/dV
 // Smem: K, V resident; Q(i), dO(i) through a 4-slot single-tile ring (Q(i) ->
 // ring index 2i, dO(i) -> 2i+1, each released by its last MMA); dS^T (bf16)
@@ -369,17 +392,16 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p1_done);  // S^T(i) read: S^T(i+1) may be issued
-#pragma unroll
-        for (int j = 0; j < NC; ++j) pv[j] = ex2_approx(fmaf(__uint_as_float(sr[j]), sl2, -sv[j]));
         if (need_mask) {
-#pragma unroll
-          for (int j = 0; j < NC; ++j) {
-            const int qrow = q0 + wg * NC + j;
-            int lo, hi;
-            row_interval(g, qseg, qrow, kseg, lo, hi);
-            const bool vis = qrow < q1 && kpos < k1 && kpos >= lo && kpos < hi;
-            pv[j] = vis ? pv[j] : 0.f;
-          }
+          // visible q rows of this key form one interval (tilemap.cuh key_interval)
+          int qa, qb;
+          key_interval(g, kseg, kpos, qseg, qa, qb);
+          if (qb > q1) qb = q1;
+          if (kpos >= k1) qb = qa;
+          const int cbase = q0 + wg * NC;
+          p_tile<true, NC>(sr, sv, sl2, qa - cbase, qb - cbase, pv);
+        } else {
+          p_tile<false, NC>(sr, sv, sl2, 0, NC, pv);
         }
       }
       TRACE(8 * (i & 127) + 2, blockIdx.x == 0 && threadIdx.x == 0);
@@ -668,12 +690,10 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         uint32_t sr[32];
         tmem_ld32(sbase + cb, sr);
         tmem_ld_wait();
-#pragma unroll
-        for (int jj = 0; jj < 32; ++jj) pv[32 * c + jj] = ex2_approx(fmaf(__uint_as_float(sr[jj]), sl2, -lse2));
-        if (need_mask) {
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) pv[32 * c + jj] = (cb + jj >= lo && cb + jj < hi) ? pv[32 * c + jj] : 0.f;
-        }
+        if (need_mask)
+          p_row<true>(sr, lse2, sl2, lo - cb, hi - cb, pv + 32 * c);
+        else
+          p_row<false>(sr, lse2, sl2, 0, 32, pv + 32 * c);
       }
       // phase 2: dS = P (dP - D) -> bf16 over the S columns already read
       mbar_wait(dp_full, j & 1);

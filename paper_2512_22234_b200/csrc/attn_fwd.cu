@@ -28,6 +28,7 @@
 #include "attn_common.h"
 
 #include <cuda_bf16.h>
+#include <cstdlib>
 
 namespace bd {
 namespace {
@@ -49,6 +50,14 @@ struct FwdCfg {
   static constexpr int kSmemBytes = NQ * kTileBytes + kStages * kTileBytes + kNumBars * 8 + 16 + 1024;
 };
 
+// Opt-in event trace (BD_TRACE=1): CTA 0 records clock64 stamps, read back by
+// bd_debug_trace_fwd().
+__device__ long long g_trace_fwd[8192];
+#define FTRACE(slot, cond)                                        \
+  do {                                                            \
+    if (a.trace && (cond)) g_trace_fwd[(slot)] = clock64();       \
+  } while (0)
+
 struct FwdArgs {
   const int* map;
   __nv_bfloat16* o;
@@ -56,7 +65,50 @@ struct FwdArgs {
   int batch, n_q_heads, n_hg, group, N;
   Geom g;
   float scale_log2;
+  int trace;
 };
+
+// One online-softmax step of a 128-column S tile held in TMEM at tS (this
+// thread's row): optional interval mask [lo, hi), running max m (log2 units,
+// lazily raised by > 8), running sum l, P = 2^(s sl2 - m) written over tS as
+// bf16.  Returns the new max, whether O must be rescaled, and by how much.
+template <bool MASKED>
+__device__ __forceinline__ void softmax_tile(uint32_t tS, int lo, int hi, float sl2, float m, float& l,
+                                             float& m_new, bool& resc, float& alpha) {
+  uint32_t sr[128];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) tmem_ld32(tS + 32 * c, sr + 32 * c);
+  tmem_ld_wait();
+  float* s = reinterpret_cast<float*>(sr);
+  if (MASKED) {
+#pragma unroll
+    for (int c = 0; c < 128; ++c) s[c] = (c >= lo && c < hi) ? s[c] : -INFINITY;
+  }
+  float mx = s[0];
+#pragma unroll
+  for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
+  const float tmax = mx * sl2;
+  m_new = m;
+  resc = false;
+  if (tmax > m + 8.f) {
+    m_new = tmax;
+    resc = true;
+  }
+  const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+  alpha = resc ? ex2_approx(m - m_use) : 1.f;
+  float sum = 0.f;
+  uint32_t pk[64];
+#pragma unroll
+  for (int c = 0; c < 64; ++c) {
+    const float p0 = ex2_mix(2 * c, fmaf(s[2 * c], sl2, -m_use));
+    const float p1 = ex2_mix(2 * c + 1, fmaf(s[2 * c + 1], sl2, -m_use));
+    sum += p0 + p1;
+    pk[c] = pack_bf16x2(p0, p1);
+  }
+  l = l * alpha + sum;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) tmem_st32(tS + 32 * c, pk + 32 * c);
+}
 
 template <int D, int NQ>
 __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
@@ -145,52 +197,55 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
     if (elect_one()) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int j = 0; j < n_kt; ++j) {
-        const int sK = stage;
-        const uint32_t phK = phase;
-        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-        const int sV = stage;
-        const uint32_t phV = phase;
-        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-        // ---- S_q = Q_q K^T
-        mbar_wait(&kv_full[sK], phK);
-        tc_fence_after();
-        const uint32_t kaddr = smem_u32(sKV + sK * C::kTileBytes);
+      // Ring index of K(j) is 2j, of V(j) 2j+1.  Issue order per tile j and head q:
+      // PV_q(j) as soon as P_q(j) is ready, then (after PV_q(j) has consumed P_q,
+      // which aliases S_q) S_q(j+1).  Heads are handled independently so the two
+      // softmax warpgroups fall into a ping-pong: one runs its exps while the
+      // other's PV / S MMAs execute.
+      auto slot = [](int idx) { return idx % C::kStages; };
+      auto ph = [](int idx) { return (uint32_t)((idx / C::kStages) & 1); };
+      auto kv_addr = [&](int idx) { return smem_u32(sKV + slot(idx) * C::kTileBytes); };
+      auto issue_s = [&](int q, int j) {
+        const uint32_t qaddr = smem_u32(sQ + q * C::kTileBytes), kaddr = kv_addr(2 * j);
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          if (j > 0) {
-            mbar_wait(&pv_done[q], (j - 1) & 1);  // P_q(j-1) (aliasing S_q) consumed
-            tc_fence_after();
-          }
-          const uint32_t qaddr = smem_u32(sQ + q * C::kTileBytes);
-#pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
-            umma_ss(tbase + C::kSCol + 128 * q, umma_desc_sw128(qaddr + off, 16, 1024),
-                    umma_desc_sw128(kaddr + off, 16, 1024), idesc_s, k > 0);
-          }
-          umma_commit(&s_full[q]);
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+          umma_ss(tbase + C::kSCol + 128 * q, umma_desc_sw128(qaddr + off, 16, 1024),
+                  umma_desc_sw128(kaddr + off, 16, 1024), idesc_s, k > 0);
         }
-        umma_commit(&kv_empty[sK]);
-        // ---- O_q += P_q V
-        mbar_wait(&kv_full[sV], phV);
-        tc_fence_after();
-        const uint32_t vaddr = smem_u32(sKV + sV * C::kTileBytes);
+        umma_commit(&s_full[q]);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&kv_full[slot(0)], ph(0));
+      tc_fence_after();
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) issue_s(q, 0);
+      umma_commit(&kv_empty[slot(0)]);
+      for (int j = 0; j < n_kt; ++j) {
+        mbar_wait(&kv_full[slot(2 * j + 1)], ph(2 * j + 1));
+        FTRACE(1024 + 8 * (j & 127) + 0, blockIdx.x == 0);
+        const uint32_t vaddr = kv_addr(2 * j + 1);
+        const bool has_next = j + 1 < n_kt;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
           mbar_wait(&p_full[q], j & 1);
+          FTRACE(1024 + 8 * (j & 127) + 1 + q, blockIdx.x == 0);
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < 8; ++k)
             umma_ts(tbase + C::kOCol + D * q, tbase + C::kSCol + 128 * q + k * 8,
                     umma_desc_sw128(vaddr + k * 2048, 16384, 1024), idesc_o, (j > 0 || k > 0) ? 1u : 0u);
           umma_commit(&pv_done[q]);
+          if (q == NQ - 1) umma_commit(&kv_empty[slot(2 * j + 1)]);  // V(j) consumed
+          if (has_next) {
+            if (q == 0) mbar_wait(&kv_full[slot(2 * j + 2)], ph(2 * j + 2));
+            mbar_wait(&pv_done[q], j & 1);  // P_q(j) (aliasing S_q) consumed
+            FTRACE(1024 + 8 * (j & 127) + 3 + q, blockIdx.x == 0);
+            tc_fence_after();
+            issue_s(q, j + 1);
+            if (q == NQ - 1) umma_commit(&kv_empty[slot(2 * j + 2)]);  // K(j+1) consumed
+          }
         }
-        umma_commit(&kv_empty[sV]);
       }
     }
   } else {
@@ -212,44 +267,21 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
       const int kt = entry_tile(ent);
       const int k0 = tile_start(g, kt), k1 = tile_end(g, kt);
       const bool need_mask = entry_kind(ent) == kKindPartial || (k1 - k0) < 128;
+      FTRACE(8 * (j & 127) + 0 + 4 * q, blockIdx.x == 0 && (threadIdx.x & 127) == 0);
       mbar_wait(&s_full[q], j & 1);
+      FTRACE(8 * (j & 127) + 1 + 4 * q, blockIdx.x == 0 && (threadIdx.x & 127) == 0);
       tc_fence_after();
-      uint32_t sr[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tS + 32 * c, sr + 32 * c);
-      tmem_ld_wait();
-      float* s = reinterpret_cast<float*>(sr);
-      if (need_mask) {
-        const bool xt = tile_seg(g, kt) != 0;
-        const int lo = (xt ? lo1 : lo0) - k0;
-        const int hi = min(xt ? hi1 : hi0, k1) - k0;
-#pragma unroll
-        for (int c = 0; c < 128; ++c) s[c] = (c >= lo && c < hi) ? s[c] : -INFINITY;
-      }
-      float mx = s[0];
-#pragma unroll
-      for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
-      const float tmax = mx * sl2;
-      float m_new = m;
-      bool resc = false;
-      if (tmax > m + 8.f) {
-        m_new = tmax;
-        resc = true;
-      }
-      const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-      const float alpha = resc ? ex2_approx(m - m_use) : 1.f;
-      float sum = 0.f;
-      uint32_t pk[64];
-#pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const float p0 = ex2_approx(fmaf(s[2 * c], sl2, -m_use));
-        const float p1 = ex2_approx(fmaf(s[2 * c + 1], sl2, -m_use));
-        sum += p0 + p1;
-        pk[c] = pack_bf16x2(p0, p1);
-      }
-      l = l * alpha + sum;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) tmem_st32(tS + 32 * c, pk + 32 * c);
+      const bool xt = tile_seg(g, kt) != 0;
+      const int lo = (xt ? lo1 : lo0) - k0;
+      const int hi = min(xt ? hi1 : hi0, k1) - k0;
+      bool resc;
+      float alpha, m_new;
+      // two separate code paths: the masked one must not be if-converted into
+      // every tile (FULL tiles need no per-element work)
+      if (need_mask)
+        softmax_tile<true>(tS, lo, hi, sl2, m, l, m_new, resc, alpha);
+      else
+        softmax_tile<false>(tS, lo, hi, sl2, m, l, m_new, resc, alpha);
       if (j > 0 && __any_sync(0xffffffffu, resc)) {
         // O_q *= alpha (PV(j-1) has completed: S_q(j) was issued after it)
 #pragma unroll
@@ -266,6 +298,7 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[q]);
+      FTRACE(8 * (j & 127) + 2 + 4 * q, blockIdx.x == 0 && (threadIdx.x & 127) == 0);
       m = m_new;
     }
     // ---- epilogue
@@ -327,6 +360,8 @@ int launch_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   a.N = g.N;
   a.g = g;
   a.scale_log2 = scale_of(p) * 1.4426950408889634f;
+  static const bool trace_on = getenv("BD_TRACE") != nullptr;
+  a.trace = trace_on ? 1 : 0;
   const long long grid = (long long)g.NT * p.batch * a.n_hg;
   if (grid > 0x7FFFFFFF) return set_error(BD_ERR_UNSUPPORTED, "grid too large");
   attn_fwd_kernel<D, NQ><<<(unsigned)grid, C::kThreads, C::kSmemBytes, stream>>>(tmQ, tmK, tmV, a);
@@ -347,3 +382,8 @@ int run_attn_fwd(const bd_problem& p, const Geom& g, const void* q, const void* 
 }
 
 }  // namespace bd
+
+extern "C" int bd_debug_trace_fwd(int64_t* host_out, int n) {
+  if (!host_out || n <= 0 || n > 8192) return BD_ERR_INVALID_ARG;
+  return bd::check_cuda(cudaMemcpyFromSymbol(host_out, bd::g_trace_fwd, n * sizeof(long long)), "trace copy");
+}

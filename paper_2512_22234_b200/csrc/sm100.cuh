@@ -219,6 +219,32 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (offloads the MUFU, which bounds the softmax at d=128):
+// x = n + r with n = rint(x) (1.5*2^23 magic), r in [-0.5, 0.5];
+// 2^r ~ 1 + r(c1 + r(c2 + r c3)) (relative-error fit, max 1.0e-4 -- far below
+// bf16's 2^-9 rounding of P); 2^n added to the exponent bits.  x is clamped
+// at -126 so the result stays >= 2^-126 (never wraps); x <= 127.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;
+  const float r = x - (t - 12582912.f);
+  float p = fmaf(0.05500893f, r, 0.24221098f);
+  p = fmaf(p, r, 0.69328293f);
+  p = fmaf(p, r, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// Split of the exps between MUFU and the FMA-pipe polynomial: element c of a
+// row uses the polynomial iff (c % kPolyMod) == kPolyMod - 1.
+#ifndef BD_POLY_MOD
+#define BD_POLY_MOD 0
+#endif
+// (c is a compile-time constant after loop unrolling, so the branch folds.)
+__device__ __forceinline__ float ex2_mix(int c, float x) {
+  if (BD_POLY_MOD > 0 && (c % BD_POLY_MOD) == BD_POLY_MOD - 1) return ex2_poly(x);
+  return ex2_approx(x);
+}
+
 // Byte offset of 16-byte chunk `chunk` (0..7) of row `row` inside a
 // 128B-swizzled tile whose rows are 128 B.
 __device__ __forceinline__ uint32_t sw128_offset(uint32_t row, uint32_t chunk) {

@@ -75,6 +75,39 @@ __host__ __device__ inline void row_interval(const Geom& g, int qseg, int row, i
   }
 }
 
+// The transpose view used by the backward's key-row threads: the packed query
+// rows of segment `qseg` that see key `key` (a packed row of segment kseg)
+// also form one interval [qa, qb) (row intervals are monotone in the row):
+//   x0 key, x0 rows:  blk(q) >= blk(k)      -> [blk(k) B, L)
+//   x0 key, xt rows:  blk(q) >= blk(k) + 1  -> clean positions >= (blk(k)+1) B
+//   xt key, xt rows:  blk(q) == blk(k)      -> its own block (clipped to xb)
+//   xt key, x0 rows:  never
+__host__ __device__ inline void key_interval(const Geom& g, int kseg, int key, int qseg, int& qa, int& qb) {
+  const int pk = kseg ? g.xb + (key - g.L) : key;
+  const int bk = pk / g.B;
+  if (qseg == 0) {
+    if (kseg) {
+      qa = qb = 0;
+    } else {
+      qa = bk * g.B;
+      qb = g.L;
+    }
+  } else {
+    int a, b;  // clean positions
+    if (kseg == 0) {
+      a = (bk + 1) * g.B;
+      b = g.L;
+    } else {
+      a = bk * g.B;
+      b = (bk + 1) * g.B < g.L ? (bk + 1) * g.B : g.L;
+    }
+    if (a < g.xb) a = g.xb;
+    qa = g.L + a - g.xb;
+    qb = g.L + b - g.xb;
+    if (qb < qa) qb = qa;
+  }
+}
+
 // Kind of tile pair (qt, kt): 0 = EMPTY, kKindFull, kKindPartial -- decided
 // over the tile's valid rows and columns, row by row.
 __host__ __device__ inline int classify_pair(const Geom& g, int qt, int kt) {

@@ -268,3 +268,31 @@ extern "C" int bd_tilemap_host_image(const bd_problem* prob, int32_t* host_out, 
   std::copy(w.begin(), w.end(), host_out);
   return BD_OK;
 }
+
+// Consistency of the two interval views used by the kernels (host, tests):
+// key k is in row r's interval (row_interval) iff row r is in key k's
+// interval (key_interval), for every packed (row, key).  Returns the number of
+// mismatches in *mismatches.
+extern "C" int bd_tilemap_selfcheck(const bd_problem* prob, int64_t* mismatches) {
+  using namespace bd;
+  int rc = validate_problem(prob);
+  if (rc) return rc;
+  if (!mismatches) return set_error(BD_ERR_INVALID_ARG, "mismatches is null");
+  const Geom g = geom_of(*prob);
+  if ((int64_t)g.N * g.N > (int64_t)1 << 26) return set_error(BD_ERR_UNSUPPORTED, "problem too large for selfcheck");
+  int64_t bad = 0;
+  for (int r = 0; r < g.N; ++r) {
+    const int qs = r >= g.L ? 1 : 0;
+    for (int k = 0; k < g.N; ++k) {
+      const int ks = k >= g.L ? 1 : 0;
+      int lo, hi, qa, qb;
+      row_interval(g, qs, r, ks, lo, hi);
+      key_interval(g, ks, k, qs, qa, qb);
+      const bool a = k >= lo && k < hi;
+      const bool b = r >= qa && r < qb;
+      bad += (a != b);
+    }
+  }
+  *mismatches = bad;
+  return BD_OK;
+}

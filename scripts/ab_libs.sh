@@ -1,0 +1,7 @@
+#!/bin/bash
+# A/B timing of alternative builds of libbdattn.so (dev helper)
+for L in scripts/libs_tmp/*.so; do
+  cp "$L" paper_2512_22234_b200/libbdattn.so
+  echo "== $L"
+  PYTHONPATH=. timeout 200 python scripts/quick_attn.py ${1:-sdar_8b}
+done

@@ -97,3 +97,13 @@ def test_tilemap_sdar_1_7b_vs_oracle_dense():
 def test_host_image_layout():
     img = bd.ops.tilemap_host_image(bd.Problem(1, 32, 64, 4, 2, 2, 64))
     assert img[0] == 0x42444D31 and img[4] == 2 and img[6] == 3
+
+
+@pytest.mark.parametrize("P,R,B,rp", [(2, 6, 2, 1), (2, 6, 2, 0), (40, 160, 8, 0), (7, 121, 128, 1), (0, 512, 256, 1),
+                                      (100, 300, 4, 0), (5, 5, 10, 0), (24, 0, 1, 0), (130, 126, 2, 1)])
+def test_row_and_key_intervals_agree(P, R, B, rp):
+    """The transpose interval view of the dK/dV kernel equals the row view."""
+    p = bd.Problem(1, P, R, B, 1, 1, 64, repeat_prompt=rp).c()
+    n = ctypes.c_int64(-1)
+    assert _lib.lib().bd_tilemap_selfcheck(ctypes.byref(p), ctypes.byref(n)) == 0
+    assert n.value == 0
