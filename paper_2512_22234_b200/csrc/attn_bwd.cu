@@ -41,31 +41,35 @@ namespace {
 constexpr float kLog2e = 1.4426950408889634f;
 
 // ------------------------------------------------------------ preprocess
-// grid: (ceil(N/4), b*Hq); block 128: each warp handles one packed row.
+// D_i = rowsum(dO_i o O_i) and log2-domain LSE, written tile-major.  One
+// 16-byte load per thread per tensor; D/8 threads per row; grid
+// (ceil(N / rows_per_block), b * Hq).
 template <int D>
-__global__ void __launch_bounds__(128) bwd_pre_kernel(const __nv_bfloat16* __restrict__ o,
+__global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __restrict__ o,
                                                       const __nv_bfloat16* __restrict__ dout,
                                                       const float* __restrict__ lse, float* __restrict__ lse2_t,
                                                       float* __restrict__ dsum_t, int N, int Hq, Geom g) {
+  constexpr int kTpr = D / 8;             // threads per row
+  constexpr int kRows = 256 / kTpr;       // rows per block
   const int bh = blockIdx.y;
   const int b = bh / Hq, h = bh - b * Hq;
-  const int n = blockIdx.x * 4 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (n >= N) return;
-  const size_t base = (((size_t)b * N + n) * Hq + h) * D;
+  const int n = blockIdx.x * kRows + threadIdx.x / kTpr;
+  const int sub = threadIdx.x % kTpr;
   float acc = 0.f;
-  constexpr int kPer = D / 32;  // elements per lane
-  const __nv_bfloat16* po = o + base + lane * kPer;
-  const __nv_bfloat16* pd = dout + base + lane * kPer;
+  if (n < N) {
+    const size_t base = (((size_t)b * N + n) * Hq + h) * D + sub * 8;
+    const uint4 a = *reinterpret_cast<const uint4*>(o + base);
+    const uint4 c = *reinterpret_cast<const uint4*>(dout + base);
+    const uint32_t av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-  for (int i = 0; i < kPer; i += 2) {
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(po + i));
-    const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(pd + i));
-    acc = fmaf(a.x, c.x, fmaf(a.y, c.y, acc));
+    for (int i = 0; i < 4; ++i) {
+      acc = fmaf(__uint_as_float(av[i] << 16), __uint_as_float(cv[i] << 16), acc);
+      acc = fmaf(__uint_as_float(av[i] & 0xFFFF0000u), __uint_as_float(cv[i] & 0xFFFF0000u), acc);
+    }
   }
 #pragma unroll
-  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) {
+  for (int off = kTpr / 2; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (n < N && sub == 0) {
     const int t = n >= g.L ? g.T0 + (n - g.L) / kTileRows : n / kTileRows;
     const int r = n - tile_start(g, t);
     const size_t slot = ((size_t)bh * g.NT + t) * kTileRows + r;
@@ -483,10 +487,11 @@ template <int D>
 struct DqCfg {
   static constexpr int kTileBytes = 128 * D * 2;
   static constexpr int kStages = 4;  // K/V ring (K(j), V(j) alternate)
-  static constexpr int kComputeWarps = 8;
-  static constexpr int kTmaWarp = 8;
-  static constexpr int kMmaWarp = 9;
-  static constexpr int kThreads = 320;
+  static constexpr int kWGs = 4;     // compute warpgroups, 32 key columns each
+  static constexpr int kComputeWarps = 4 * kWGs;
+  static constexpr int kTmaWarp = kComputeWarps;
+  static constexpr int kMmaWarp = kComputeWarps + 1;
+  static constexpr int kThreads = 32 * (kComputeWarps + 2);
   static constexpr int kColS0 = 0, kColS1 = 128, kColDP = 256, kColDQ = 384;
   static constexpr uint32_t kTmemCols = 512;
   static constexpr int kOffQ = 0;
@@ -640,12 +645,12 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         }
         mbar_wait(compute_done, j & 1);
         tc_fence_after();
-        // dQ += dS(j) K(j): A = dS bf16 in S[j&1] (keys 0..63 at +0, 64..127 at +64)
+        // dQ += dS(j) K(j): A = dS bf16 in S[j&1]; keys 32w..32w+31 at cols 32w..32w+15
         const uint32_t sbase = tbase + ((j & 1) ? C::kColS1 : C::kColS0);
         const uint32_t kaddr = ring(2 * j);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          umma_ts(tbase + C::kColDQ, sbase + (k < 4 ? k * 8 : 64 + (k - 4) * 8),
+          umma_ts(tbase + C::kColDQ, sbase + 32 * (k >> 1) + 8 * (k & 1),
                   umma_desc_sw128(kaddr + k * 2048, 16384, 1024), idesc_q, (j > 0 || k > 0) ? 1u : 0u);
         umma_commit(dq_done);
         umma_commit(&kv_empty[slot(2 * j)]);  // K(j) consumed
@@ -682,41 +687,35 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
       const uint32_t sbase = tbase + lane_off + ((j & 1) ? C::kColS1 : C::kColS0);
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
-      // phase 1: P = exp2(S sl2 - lse2) for this warpgroup's 64 key columns
-      float pv[64];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int cb = wg * 64 + c * 32;
+      // phase 1: P = exp2(S sl2 - lse2) for this warpgroup's 32 key columns
+      const int cb = wg * 32;
+      float pv[32];
+      {
         uint32_t sr[32];
         tmem_ld32(sbase + cb, sr);
         tmem_ld_wait();
         if (need_mask)
-          p_row<true>(sr, lse2, sl2, lo - cb, hi - cb, pv + 32 * c);
+          p_row<true>(sr, lse2, sl2, lo - cb, hi - cb, pv);
         else
-          p_row<false>(sr, lse2, sl2, 0, 32, pv + 32 * c);
+          p_row<false>(sr, lse2, sl2, 0, 32, pv);
       }
       // phase 2: dS = P (dP - D) -> bf16 over the S columns already read
       mbar_wait(dp_full, j & 1);
       tc_fence_after();
-      uint32_t pk[32];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int cb = wg * 64 + c * 32;
+      uint32_t pk[16];
+      {
         uint32_t dr[32];
         tmem_ld32(tbase + lane_off + C::kColDP + cb, dr);
         tmem_ld_wait();
-        if (c == 1) {  // dP(j) fully read: the MMA warp may overwrite it with dP(j+1)
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(dp_free);
-        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dp_free);  // dP(j) read: dP(j+1) may be issued
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj)
-          pk[16 * c + jj] = pack_bf16x2(pv[32 * c + 2 * jj] * (__uint_as_float(dr[2 * jj]) - dsum),
-                                        pv[32 * c + 2 * jj + 1] * (__uint_as_float(dr[2 * jj + 1]) - dsum));
+          pk[jj] = pack_bf16x2(pv[2 * jj] * (__uint_as_float(dr[2 * jj]) - dsum),
+                               pv[2 * jj + 1] * (__uint_as_float(dr[2 * jj + 1]) - dsum));
       }
-      tmem_st16(sbase + wg * 64, pk);
-      tmem_st16(sbase + wg * 64 + 16, pk + 16);
+      tmem_st16(sbase + cb, pk);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -726,14 +725,15 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
     mbar_wait(acc_done, 0);
     tc_fence_after();
     const bool ok = row < q1;
-    __nv_bfloat16* out = a.dq + (((size_t)b * a.N + row) * a.n_q_heads + h) * D + wg * (D / 2);
-#pragma unroll
-    for (int c = 0; c < D / 64; ++c) {
-      uint32_t v[32];
-      tmem_ld32(tbase + lane_off + C::kColDQ + wg * (D / 2) + 32 * c, v);
-      tmem_ld_wait();
-      store_row_bf16(out + 32 * c, v, a.scale, ok);
-    }
+    constexpr int DC = D / C::kWGs;
+    __nv_bfloat16* out = a.dq + (((size_t)b * a.N + row) * a.n_q_heads + h) * D + wg * DC;
+    uint32_t v[32];
+    if (DC == 32)
+      tmem_ld32(tbase + lane_off + C::kColDQ + wg * DC, v);
+    else
+      tmem_ld16(tbase + lane_off + C::kColDQ + wg * DC, v);
+    tmem_ld_wait();
+    store_row_bf16_n<DC>(out, v, a.scale, ok);
   }
   tc_fence_before();
   __syncthreads();
@@ -760,8 +760,9 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   // 1. preprocess: D and log2 LSE, tile-major (pad rows zeroed)
   zero_kernel<<<296, 256, 0, stream>>>(reinterpret_cast<float4*>(vec_ws), 2 * nvec / 4);
   {
-    dim3 grid((g.N + 3) / 4, p.batch * Hq);
-    bwd_pre_kernel<D><<<grid, 128, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
+    constexpr int kRows = 256 / (D / 8);
+    dim3 grid((g.N + kRows - 1) / kRows, p.batch * Hq);
+    bwd_pre_kernel<D><<<grid, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
                                                  reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2_t, dsum_t,
                                                  g.N, Hq, g);
   }

@@ -93,15 +93,15 @@ __device__ void block_exclusive_scan(const int* cnt, int* out, int n, int* scrat
   __syncthreads();
 }
 
-// Warp-cooperative classification (same result as classify_pair).
-__device__ int classify_pair_warp(const Geom& g, int qt, int kt) {
-  const int q0 = tile_start(g, qt), q1 = tile_end(g, qt), qs = tile_seg(g, qt);
-  const int k0 = tile_start(g, kt), k1 = tile_end(g, kt), ks = tile_seg(g, kt);
+// Warp-cooperative classification of (qt, kt) from the per-row intervals of
+// q-tile qt held in shared memory (lo/hi for key segment ks); same result as
+// classify_pair.
+__device__ int classify_pair_warp(const Geom& g, int qt, int kt, const int* s_lo, const int* s_hi) {
+  const int nrow = tile_end(g, qt) - tile_start(g, qt);
+  const int k0 = tile_start(g, kt), k1 = tile_end(g, kt);
   bool any = false, all = true;
-  for (int r = q0 + (int)(threadIdx.x & 31); r < q1; r += 32) {
-    int lo, hi;
-    row_interval(g, qs, r, ks, lo, hi);
-    const int a = max(lo, k0), b = min(hi, k1);
+  for (int r = (int)(threadIdx.x & 31); r < nrow; r += 32) {
+    const int a = max(s_lo[r], k0), b = min(s_hi[r], k1);
     if (b > a) any = true;
     if (!(a == k0 && b == k1)) all = false;
   }
@@ -110,59 +110,66 @@ __device__ int classify_pair_warp(const Geom& g, int qt, int kt) {
   return any ? (all ? kKindFull : kKindPartial) : 0;
 }
 
+// One warp per q-tile (strided).  Shared memory: rowlen[NT], collen[NT],
+// colfill[NT], scan scratch[1024], and per warp 4 x 128 ints of row intervals.
 __global__ void __launch_bounds__(kBuildThreads, 1) build_map_kernel(Geom g, int* __restrict__ ws) {
   extern __shared__ int sh[];
   const int NT = g.NT;
-  int* rowlen = sh;              // NT
-  int* collen = sh + NT;         // NT
-  int* scratch = sh + 2 * NT;    // kBuildThreads
+  int* rowlen = sh;                 // NT
+  int* collen = sh + NT;            // NT
+  int* colfill = sh + 2 * NT;       // NT
+  int* scratch = sh + 3 * NT;       // kBuildThreads
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = kBuildThreads / 32;
+  int* wiv = sh + 3 * NT + kBuildThreads + warp * 512;  // this warp's row intervals
   const int cap = map_capacity(g);
   MapView mv{ws, NT, cap};
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = kBuildThreads / 32;
-  for (int i = tid; i < NT; i += kBuildThreads) collen[i] = 0;
-  // pass 1: row lengths
-  for (int t = warp; t < NT; t += nwarps) {
-    int n = 0;
-    for (int ks = 0; ks < 2; ++ks) {
-      int a, b;
-      candidate_range(g, t, ks, a, b);
-      for (int kt = a; kt < b; ++kt) n += classify_pair_warp(g, t, kt) ? 1 : 0;
-    }
-    if (lane == 0) rowlen[t] = n;
+  for (int i = tid; i < NT; i += kBuildThreads) {
+    collen[i] = 0;
+    colfill[i] = 0;
   }
   __syncthreads();
-  block_exclusive_scan(rowlen, mv.row_ptr(), NT, scratch);
-  // pass 2: fill row entries, count columns
-  for (int t = warp; t < NT; t += nwarps) {
-    int n = mv.row_ptr()[t];
-    for (int ks = 0; ks < 2; ++ks) {
-      int a, b;
-      candidate_range(g, t, ks, a, b);
-      for (int kt = a; kt < b; ++kt) {
-        const int kind = classify_pair_warp(g, t, kt);
-        if (kind) {
-          if (lane == 0) {
-            mv.row_ent()[n] = entry_make(kt, kind);
-            atomicAdd(&collen[kt], 1);
+  // passes 1 and 2: classify candidate k-tiles of each q-tile; count, then fill
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int t = warp; t < NT; t += nwarps) {
+      const int q0 = tile_start(g, t), nrow = tile_end(g, t) - q0, qs = tile_seg(g, t);
+      for (int r = lane; r < nrow; r += 32) {
+        row_interval(g, qs, q0 + r, 0, wiv[r], wiv[128 + r]);
+        row_interval(g, qs, q0 + r, 1, wiv[256 + r], wiv[384 + r]);
+      }
+      __syncwarp();
+      int n = pass ? mv.row_ptr()[t] : 0;
+      for (int ks = 0; ks < 2; ++ks) {
+        int a, b;
+        candidate_range(g, t, ks, a, b);
+        for (int kt = a; kt < b; ++kt) {
+          const int kind = classify_pair_warp(g, t, kt, wiv + 256 * ks, wiv + 256 * ks + 128);
+          if (kind) {
+            if (pass && lane == 0) {
+              mv.row_ent()[n] = entry_make(kt, kind);
+              atomicAdd(&collen[kt], 1);
+            }
+            ++n;
           }
-          ++n;
         }
       }
+      if (!pass && lane == 0) rowlen[t] = n;
+      __syncwarp();
     }
+    __syncthreads();
+    if (!pass) block_exclusive_scan(rowlen, mv.row_ptr(), NT, scratch);
   }
-  __syncthreads();
   block_exclusive_scan(collen, mv.col_ptr(), NT, scratch);
-  // pass 3: column entries in increasing q-tile order (binary search in rows)
-  for (int kt = tid; kt < NT; kt += kBuildThreads) {
-    int o = mv.col_ptr()[kt];
+  // pass 3: column entries in increasing q-tile order -- warp 0 walks the rows
+  // in order, lanes take a row's entries (each k-tile appears once per row)
+  if (warp == 0) {
     for (int t = 0; t < NT; ++t) {
-      int lo = mv.row_ptr()[t], hi = mv.row_ptr()[t + 1];
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (entry_tile(mv.row_ent()[mid]) < kt) lo = mid + 1; else hi = mid;
+      const int e0 = mv.row_ptr()[t], e1 = mv.row_ptr()[t + 1];
+      for (int e = e0 + lane; e < e1; e += 32) {
+        const int ent = mv.row_ent()[e];
+        const int kt = entry_tile(ent);
+        mv.col_ent()[mv.col_ptr()[kt] + colfill[kt]++] = entry_make(t, entry_kind(ent));
       }
-      if (lo < mv.row_ptr()[t + 1] && entry_tile(mv.row_ent()[lo]) == kt)
-        mv.col_ent()[o++] = entry_make(t, entry_kind(mv.row_ent()[lo]));
+      __syncwarp();
     }
   }
   // pass 4: longest-first orders (stable: ties by index)
@@ -195,11 +202,11 @@ __global__ void __launch_bounds__(kBuildThreads, 1) build_map_kernel(Geom g, int
 }  // namespace
 
 int build_map_device(const Geom& g, int* ws, cudaStream_t stream) {
-  const size_t smem = (2 * (size_t)g.NT + kBuildThreads) * sizeof(int);
+  const size_t smem = (3 * (size_t)g.NT + kBuildThreads + (kBuildThreads / 32) * 512) * sizeof(int);
   if (g.NT > kMaxTiles) return set_error(BD_ERR_UNSUPPORTED, "too many tiles (%d > %d)", g.NT, kMaxTiles);
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(build_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(build_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_done = true;
   }
   build_map_kernel<<<1, kBuildThreads, smem, stream>>>(g, ws);
