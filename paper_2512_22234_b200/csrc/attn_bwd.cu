@@ -220,11 +220,12 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
   const Geom& g = a.g;
   if ((smem_u32(smem) & 1023u) != 0) __trap();
 
-  const int per_tile = a.batch * a.n_kv_heads;
-  const int rank = blockIdx.x / per_tile;
-  const int rem = blockIdx.x - rank * per_tile;
-  const int b = rem / a.n_kv_heads;
-  const int kvh = rem - b * a.n_kv_heads;
+  // Grid order: (sequence, kv head) outermost, LPT rank of the k-tile inner --
+  // concurrently resident CTAs stream the same Q / dO tiles (L2 reuse).
+  const int unit = blockIdx.x / g.NT;
+  const int rank = blockIdx.x - unit * g.NT;
+  const int b = unit / a.n_kv_heads;
+  const int kvh = unit - b * a.n_kv_heads;
   const MapView mv{const_cast<int*>(a.map), g.NT, map_capacity(g)};
   const int kt = mv.bwd_order()[rank];
   const int e0 = mv.col_ptr()[kt];
@@ -529,12 +530,15 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
   const Geom& g = a.g;
   if ((smem_u32(smem) & 1023u) != 0) __trap();
 
-  const int per_tile = a.batch * a.n_q_heads;
-  const int rank = blockIdx.x / per_tile;
-  const int rem = blockIdx.x - rank * per_tile;
-  const int b = rem / a.n_q_heads;
-  const int h = rem - b * a.n_q_heads;
-  const int kvh = h / a.group;
+  // Grid order: (sequence, kv head) outermost, then the q-tile's LPT rank,
+  // then the q-heads of the group (they share every K/V tile: L2 reuse).
+  const int per_unit = g.NT * a.group;
+  const int unit = blockIdx.x / per_unit;
+  const int rem = blockIdx.x - unit * per_unit;
+  const int rank = rem / a.group;
+  const int b = unit / a.n_kv_heads;
+  const int kvh = unit - b * a.n_kv_heads;
+  const int h = kvh * a.group + (rem - rank * a.group);
   const MapView mv{const_cast<int*>(a.map), g.NT, map_capacity(g)};
   const int qt = mv.fwd_order()[rank];
   const int e0 = mv.row_ptr()[qt];

@@ -62,7 +62,7 @@ struct FwdArgs {
   const int* map;
   __nv_bfloat16* o;
   float* lse;
-  int batch, n_q_heads, n_hg, group, N;
+  int batch, n_q_heads, n_hg, group, N, n_kv;
   Geom g;
   float scale_log2;
   int trace;
@@ -132,12 +132,17 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
   const Geom& g = a.g;
 
   // ---- work unit: LPT rank of the q-tile, then (sequence, head pair)
-  const int per_tile = a.batch * a.n_hg;
-  const int rank = blockIdx.x / per_tile;
-  const int rem = blockIdx.x - rank * per_tile;
-  const int b = rem / a.n_hg;
-  const int h0 = (rem - b * a.n_hg) * NQ;
-  const int kvh = h0 / a.group;
+  // Grid order: (sequence, kv head) outermost, then the q-tile's LPT rank,
+  // then the head pairs of the group -- concurrently resident CTAs belong to
+  // the same (sequence, kv head) and stream the same K/V tiles (L2 reuse).
+  const int hp_per_kv = a.group / NQ;
+  const int per_unit = g.NT * hp_per_kv;
+  const int unit = blockIdx.x / per_unit;
+  const int rem = blockIdx.x - unit * per_unit;
+  const int rank = rem / hp_per_kv;
+  const int b = unit / a.n_kv;
+  const int kvh = unit - b * a.n_kv;
+  const int h0 = kvh * a.group + (rem - rank * hp_per_kv) * NQ;
   const MapView mv{const_cast<int*>(a.map), g.NT, map_capacity(g)};
   const int qt = mv.fwd_order()[rank];
   const int e0 = mv.row_ptr()[qt];
@@ -357,6 +362,7 @@ int launch_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   a.n_q_heads = p.n_q_heads;
   a.n_hg = p.n_q_heads / NQ;
   a.group = p.n_q_heads / p.n_kv_heads;
+  a.n_kv = p.n_kv_heads;
   a.N = g.N;
   a.g = g;
   a.scale_log2 = scale_of(p) * 1.4426950408889634f;
