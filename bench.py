@@ -277,9 +277,11 @@ def run_ours(args):
     fwd_achieved = fwd_f / (phase["attn_fwd"] * 1e-3) / 1e12
     lp_bytes = step.n_rows * step.V * 2
     traffic = load_traffic()
-    roofline = {"kernel": "bd_attn_bwd (attn_bwd_kernel + pre/convert)", "bound": "tensor",
+    roofline = {"kernel": "bd_attn_bwd (attn_bwd_dkdv_kernel + attn_bwd_dq_kernel + bwd_pre + tile map)",
+                "bound": "tensor",
                 "achieved": round(bwd_achieved, 1), "peak": peak_s, "unit": "TFLOP/s",
-                "frac": round(bwd_achieved / peak_s, 4), "traffic": traffic.get("attn_bwd_kernel"),
+                "frac": round(bwd_achieved / peak_s, 4), "traffic": traffic.get("attn_bwd"),
+                "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/ncu_traffic.json)",
                 "peak_kind": f"bf16 sustained ({peak_src}); kernel timed inside a long step",
                 "algorithmic": f"useful bwd FLOPs per launch = 10 d Hq b L(L+B) = {bwd_f:.4e}"}
     others = {
@@ -292,11 +294,12 @@ def run_ours(args):
         "logprob": {"bound": "hbm", "achieved": round(lp_bytes / (phase["logprob"] * 1e-3) / 1e9, 1),
                     "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": round(lp_bytes / (phase["logprob"] * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
-                    "traffic": traffic.get("logprob_kernel")},
+                    "traffic": (traffic["logprob_ratio"] * lp_bytes) if "logprob_ratio" in traffic else None},
         "logprob_bwd": {"bound": "hbm", "achieved": round(2 * lp_bytes / (phase["logprob_bwd"] * 1e-3) / 1e9, 1),
                         "peak": peaks["hbm_gbs"], "unit": "GB/s",
                         "frac": round(2 * lp_bytes / (phase["logprob_bwd"] * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
-                        "traffic": traffic.get("logprob_bwd_kernel")},
+                        "traffic": (traffic["logprob_bwd_ratio"] * 2 * lp_bytes)
+                        if "logprob_bwd_ratio" in traffic else None},
     }
     clocks = clk.summary()
     line = {
