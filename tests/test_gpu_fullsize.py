@@ -1,0 +1,117 @@
+"""GPU parity at BASELINE.json's full sizes (SDAR-1.7B and SDAR-8B shapes), in
+the launch configuration bench.py times (same ABI calls, full batch), checked on
+sampled outputs the fp64 oracle computes one by one:
+
+* O / LSE / dQ for sampled query rows of sampled (sequence, head) pairs --
+  oracle.attention.forward_rows / backward_rows;
+* dK / dV for sampled keys of a sampled (sequence, kv head): the sum over the
+  group's q-heads of backward_rows restricted to exactly the rows that see the
+  key (rows that do not see a key contribute nothing to its gradient);
+* logp / LSE for sampled rows of the full 131,072 x 151,936 logits.
+
+Inputs are seeded torch RNG draws on the device (workloads.attn_inputs); the
+oracle receives host copies of the slices it needs.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2512_22234_b200 as bd
+from paper_2512_22234_b200 import ops
+from oracle import Problem as OProblem, attention, mask, logprob as olp
+from parity import FWD_MAX_ABS, FWD_REL_L2, GRAD_REL_L2, LOGP_MAX_ABS, metrics, t2np
+from workloads import CONFIGS, attn_inputs, logits_inputs, VOCAB_QWEN3
+
+
+def _oprob(cfg):
+    return OProblem(cfg.batch, cfg.prompt_len, cfg.response_len, cfg.block_size, cfg.n_q_heads,
+                    cfg.n_kv_heads, cfg.head_dim, cfg.repeat_prompt)
+
+
+def _rows(cfg, n, seed):
+    g = np.random.default_rng(seed)
+    N, L = cfg.ntot, cfg.L
+    fixed = [0, 1, L - 1, L, N - 1]  # segment ends
+    return np.unique(np.concatenate([fixed, g.integers(0, N, n)]))
+
+
+def _slice(x, b, h):
+    return x[b:b + 1, :, h:h + 1, :].float().cpu()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["sdar_1_7b", "sdar_8b"])
+def test_fullsize_sampled_parity(cuda_ok, name):
+    cfg = CONFIGS[name]
+    prob = bd.Problem.from_cfg(cfg)
+    q, k, v, do = attn_inputs(cfg, device="cuda")
+    o, lse = bd.attn_fwd(prob, q, k, v)
+    dq, dk, dv = bd.attn_bwd(prob, q, k, v, o, lse, do)
+    torch.cuda.synchronize()
+    G = cfg.n_q_heads // cfg.n_kv_heads
+    one = OProblem(1, cfg.prompt_len, cfg.response_len, cfg.block_size, 1, 1, cfg.head_dim, cfg.repeat_prompt)
+    rng = np.random.default_rng(7)
+    # -- rows: (b, h) = (0, 0), (b-1, Hq-1), one random
+    pairs = [(0, 0), (cfg.batch - 1, cfg.n_q_heads - 1), (int(rng.integers(cfg.batch)), int(rng.integers(cfg.n_q_heads)))]
+    got_o, ref_o, got_l, ref_l, got_dq, ref_dq = [], [], [], [], [], []
+    for (b, h) in pairs:
+        g_ = h // G
+        rows = _rows(cfg, 96, b * 131 + h)
+        qs, ks, vs, dos = _slice(q, b, h), _slice(k, b, g_), _slice(v, b, g_), _slice(do, b, h)
+        o_r, l_r = attention.forward_rows(one, qs, ks, vs, 0, 0, rows)
+        dq_r, _, _ = attention.backward_rows(one, qs, ks, vs, dos, 0, 0, rows)
+        got_o.append(t2np(o[b, rows, h]))
+        ref_o.append(o_r)
+        got_l.append(t2np(lse[b, h, rows]))
+        ref_l.append(l_r)
+        got_dq.append(t2np(dq[b, rows, h]))
+        ref_dq.append(dq_r)
+    mo = metrics(np.concatenate(got_o), np.concatenate(ref_o))
+    ml = metrics(np.concatenate(got_l), np.concatenate(ref_l))
+    mq = metrics(np.concatenate(got_dq), np.concatenate(ref_dq))
+    print(name, "O", mo, "LSE", ml, "dQ", mq)
+    assert mo["finite"] and mo["max_abs"] <= FWD_MAX_ABS and mo["rel_l2"] <= FWD_REL_L2
+    assert ml["finite"] and ml["max_abs"] <= FWD_MAX_ABS and ml["rel_l2"] <= FWD_REL_L2
+    assert mq["finite"] and mq["rel_l2"] <= GRAD_REL_L2
+    # -- keys of one (sequence, kv head): last x0 block, a middle x0 key, xt keys
+    b, g_ = cfg.batch - 1, cfg.n_kv_heads - 1
+    L, N, B = cfg.L, cfg.ntot, cfg.block_size
+    keys = np.array([L - 1, L - B, L // 2 + 3, L + 5, N - 1, L + L // 2])
+    vis = mask.mask_rows(one, np.arange(N))[:, keys]  # [N, n_keys]
+    ks, vs = _slice(k, b, g_), _slice(v, b, g_)
+    ref_dk = np.zeros((len(keys), cfg.head_dim))
+    ref_dv = np.zeros((len(keys), cfg.head_dim))
+    for hh in range(G):
+        h = g_ * G + hh
+        qs, dos = _slice(q, b, h), _slice(do, b, h)
+        for j in range(len(keys)):
+            rows = np.where(vis[:, j])[0]
+            _, dk_p, dv_p = attention.backward_rows(one, qs, ks, vs, dos, 0, 0, rows)
+            ref_dk[j] += dk_p[keys[j]]
+            ref_dv[j] += dv_p[keys[j]]
+    mk = metrics(t2np(dk[b, keys, g_]), ref_dk)
+    mv = metrics(t2np(dv[b, keys, g_]), ref_dv)
+    print(name, "dK", mk, "dV", mv)
+    assert mk["finite"] and mk["rel_l2"] <= GRAD_REL_L2
+    assert mv["finite"] and mv["rel_l2"] <= GRAD_REL_L2
+
+
+@pytest.mark.gpu
+def test_fullsize_logprob_sampled(cuda_ok):
+    """bd_logprob over the full SDAR-8B logits (b R = 131,072 rows x 151,936)."""
+    cfg = CONFIGS["sdar_8b"]
+    n = cfg.batch * cfg.response_len
+    V = VOCAB_QWEN3
+    z = torch.empty((n, V), dtype=torch.bfloat16, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for r0 in range(0, n, 4096):
+        z[r0:r0 + 4096] = torch.randn((min(4096, n - r0), V), generator=g, device="cuda") * 3.0
+    t = torch.randint(0, V, (n,), generator=g, device="cuda", dtype=torch.int32)
+    logp, lse = ops.logprob(z, t)
+    torch.cuda.synchronize()
+    rows = np.unique(np.concatenate([[0, n - 1], np.random.default_rng(3).integers(0, n, 256)]))
+    ref_lp, ref_lse = olp.logprob(z[rows].float().cpu(), t[rows].long().cpu())
+    m = metrics(t2np(logp[rows]), ref_lp)
+    assert m["finite"] and m["max_abs"] <= LOGP_MAX_ABS, m
+    assert metrics(t2np(lse[rows]), ref_lse)["max_abs"] <= LOGP_MAX_ABS
