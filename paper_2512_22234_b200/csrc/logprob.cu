@@ -55,23 +55,53 @@ __global__ void __launch_bounds__(kThreads) logprob_kernel(int64_t n_rows, int V
   const bool vec = ((reinterpret_cast<uintptr_t>(zr) & 15) == 0) && (V % 8 == 0);
   float m = -INFINITY, s = 0.f;
   if (vec) {
+    // Running max m is only raised (and s rescaled) when a 16-element chunk
+    // exceeds it, so the steady state costs one FFMA + one ex2 per element.
     const int nv = V / 8;
-    for (int i = tid; i < nv; i += kThreads) {
-      const ulonglong2 u = ld_stream(zr + 8 * i);
-      const uint32_t w[4] = {(uint32_t)u.x, (uint32_t)(u.x >> 32), (uint32_t)u.y, (uint32_t)(u.y >> 32)};
-      float x[8];
+    auto chunk = [&](const ulonglong2& u0, const ulonglong2& u1) {
+      const uint32_t w[8] = {(uint32_t)u0.x, (uint32_t)(u0.x >> 32), (uint32_t)u0.y, (uint32_t)(u0.y >> 32),
+                             (uint32_t)u1.x, (uint32_t)(u1.x >> 32), (uint32_t)u1.y, (uint32_t)(u1.y >> 32)};
+      float z[16];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        x[2 * j] = __uint_as_float(w[j] << 16) * kLog2e;
-        x[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u) * kLog2e;
+      for (int j = 0; j < 8; ++j) {
+        z[2 * j] = __uint_as_float(w[j] << 16);
+        z[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
       }
-      float mx = x[0];
+      float mx = z[0];
 #pragma unroll
-      for (int j = 1; j < 8; ++j) mx = fmaxf(mx, x[j]);
+      for (int j = 1; j < 16; ++j) mx = fmaxf(mx, z[j]);
+      mx *= kLog2e;
+      if (mx > m) {
+        s *= ex2_approx(m - mx);  // m = -inf -> 0
+        m = mx;
+      }
       float acc = 0.f;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc += ex2_approx(x[j] - mx);
-      online_merge(m, s, mx, acc);
+      for (int j = 0; j < 16; ++j) acc += ex2_approx(fmaf(z[j], kLog2e, -m));
+      s += acc;
+    };
+    int i = tid;
+    for (; i + kThreads < nv; i += 2 * kThreads) chunk(ld_stream(zr + 8 * i), ld_stream(zr + 8 * (i + kThreads)));
+    if (i < nv) {
+      // odd tail: one 8-element vector
+      const ulonglong2 u = ld_stream(zr + 8 * i);
+      const uint32_t w[4] = {(uint32_t)u.x, (uint32_t)(u.x >> 32), (uint32_t)u.y, (uint32_t)(u.y >> 32)};
+      float z[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        z[2 * j] = __uint_as_float(w[j] << 16);
+        z[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+      }
+      float mx = z[0];
+#pragma unroll
+      for (int j = 1; j < 8; ++j) mx = fmaxf(mx, z[j]);
+      mx *= kLog2e;
+      if (mx > m) {
+        s *= ex2_approx(m - mx);
+        m = mx;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += ex2_approx(fmaf(z[j], kLog2e, -m));
     }
   } else {
     for (int i = tid; i < V; i += kThreads) online_add(m, s, __bfloat162float(zr[i]) * kLog2e);
