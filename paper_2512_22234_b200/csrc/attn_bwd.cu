@@ -487,7 +487,10 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
 template <int D>
 struct DqCfg {
   static constexpr int kTileBytes = 128 * D * 2;
-  static constexpr int kStages = 4;  // K/V ring (K(j), V(j) alternate)
+  // K tiles live from S(j) to dQ(j), V tiles only until dP(j): separate rings,
+  // K(j) -> slot j % 3, V(j) -> slot 3 + j % 2 (ring index 2j / 2j+1).
+  static constexpr int kKSlots = 3, kVSlots = 2;
+  static constexpr int kStages = kKSlots + kVSlots;
   static constexpr int kWGs = 4;     // compute warpgroups, 32 key columns each
   static constexpr int kComputeWarps = 4 * kWGs;
   static constexpr int kTmaWarp = kComputeWarps;
@@ -503,6 +506,18 @@ struct DqCfg {
   static constexpr int kNumBars = 1 + 2 * kStages + 7;
   static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16;
 };
+
+// ring index 2j = K(j), 2j+1 = V(j)
+template <class C>
+__device__ __forceinline__ int dq_ring_slot(int idx) {
+  const int j = idx >> 1;
+  return (idx & 1) ? C::kKSlots + j % C::kVSlots : j % C::kKSlots;
+}
+template <class C>
+__device__ __forceinline__ uint32_t dq_ring_phase(int idx) {
+  const int j = idx >> 1;
+  return (uint32_t)(((idx & 1) ? j / C::kVSlots : j / C::kKSlots) & 1);
+}
 
 template <int D>
 __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
@@ -575,21 +590,16 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         tma_load_4d(sQ + kb * 16384, &tmQ, q_full, kb * 64, h, q0, b);
         tma_load_4d(sDO + kb * 16384, &tmDO, q_full, kb * 64, h, q0, b);
       }
-      int stage = 0;
-      uint32_t phase = 0;
       for (int j = 0; j < n_kt; ++j) {
         const int k0 = tile_start(g, entry_tile(ents[j]));
 #pragma unroll
         for (int kv = 0; kv < 2; ++kv) {
-          mbar_wait(&kv_empty[stage], phase ^ 1);
+          const int stage = dq_ring_slot<C>(2 * j + kv);
+          mbar_wait(&kv_empty[stage], dq_ring_phase<C>(2 * j + kv) ^ 1);
           mbar_expect_tx(&kv_full[stage], C::kTileBytes);
           uint8_t* dst = sRing + stage * C::kTileBytes;
           for (int kb = 0; kb < D / 64; ++kb)
             tma_load_4d(dst + kb * 16384, kv ? &tmV : &tmK, &kv_full[stage], kb * 64, kvh, k0, b);
-          if (++stage == C::kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
       }
     }
@@ -599,9 +609,8 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);  // S = Q K^T, dP = dO V^T
       constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, false, true);     // dQ += dS K (B MN-major)
       const uint32_t qaddr = smem_u32(sQ), doaddr = smem_u32(sDO);
-      // ring slot of K(j) is 2j mod S, of V(j) is 2j+1 mod S; phase = (2j / S) & 1 ...
-      auto slot = [&](int idx) { return idx % C::kStages; };
-      auto ph = [&](int idx) { return (uint32_t)((idx / C::kStages) & 1); };
+      auto slot = [&](int idx) { return dq_ring_slot<C>(idx); };
+      auto ph = [&](int idx) { return dq_ring_phase<C>(idx); };
       auto ring = [&](int idx) { return smem_u32(sRing + slot(idx) * C::kTileBytes); };
       auto issue_s = [&](int j) {
         const uint32_t kaddr = ring(2 * j);
@@ -642,12 +651,14 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
       }
       for (int j = 0; j < n_kt; ++j) {
         mbar_wait(dp_free, j & 1);
+        TRACE(5120 + 8 * (j & 127) + 0, blockIdx.x == 0);
         if (j + 1 < n_kt) {
           mbar_wait(&kv_full[slot(2 * j + 3)], ph(2 * j + 3));
           tc_fence_after();
           issue_dp(j + 1);
         }
         mbar_wait(compute_done, j & 1);
+        TRACE(5120 + 8 * (j & 127) + 1, blockIdx.x == 0);
         tc_fence_after();
         // dQ += dS(j) K(j): A = dS bf16 in S[j&1]; keys 32w..32w+31 at cols 32w..32w+15
         const uint32_t sbase = tbase + ((j & 1) ? C::kColS1 : C::kColS0);
@@ -661,6 +672,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         if (j + 2 < n_kt) {
           mbar_wait(&kv_full[slot(2 * j + 4)], ph(2 * j + 4));
           mbar_wait(dq_done, j & 1);  // dS(j) in S[j&1] consumed
+          TRACE(5120 + 8 * (j & 127) + 2, blockIdx.x == 0);
           tc_fence_after();
           issue_s(j + 2);
         }
@@ -690,6 +702,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
       const int hi = min(xt ? hi1 : hi0, k1) - k0;
       const uint32_t sbase = tbase + lane_off + ((j & 1) ? C::kColS1 : C::kColS0);
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      TRACE(4096 + 8 * (j & 127) + 0, blockIdx.x == 0 && threadIdx.x == 0);
       tc_fence_after();
       // phase 1: P = exp2(S sl2 - lse2) for this warpgroup's 32 key columns
       const int cb = wg * 32;
@@ -705,6 +718,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
       }
       // phase 2: dS = P (dP - D) -> bf16 over the S columns already read
       mbar_wait(dp_full, j & 1);
+      TRACE(4096 + 8 * (j & 127) + 1, blockIdx.x == 0 && threadIdx.x == 0);
       tc_fence_after();
       uint32_t pk[16];
       {
@@ -714,6 +728,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(dp_free);  // dP(j) read: dP(j+1) may be issued
+        TRACE(4096 + 8 * (j & 127) + 2, blockIdx.x == 0 && threadIdx.x == 0);
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj)
           pk[jj] = pack_bf16x2(pv[2 * jj] * (__uint_as_float(dr[2 * jj]) - dsum),
@@ -724,6 +739,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(compute_done);
+      TRACE(4096 + 8 * (j & 127) + 3, blockIdx.x == 0 && threadIdx.x == 0);
     }
     // ---- epilogue: dQ = scale * acc -> bf16
     mbar_wait(acc_done, 0);
