@@ -16,9 +16,10 @@ torch.cuda.synchronize()
 buf = (ctypes.c_int64 * 8192)()
 _lib.lib().bd_debug_trace(buf, 8192)
 t = list(buf)
-print("compute: s_full dp_full dp_read done | mma: dp_free compute_done dq_done(S issue) | period")
+print("compute(j): s_full p1end dp_full dp_read done | mma: dP(j) issue, dQ(j) issue, S(j) issue | period (dP issues)")
 for j in range(20, 34):
-    c = t[4096 + 8 * j: 4096 + 8 * j + 4]
+    c = t[4096 + 8 * j: 4096 + 8 * j + 5]
+    c = [c[0], c[4], c[1], c[2], c[3]]
     m = t[5120 + 8 * j: 5120 + 8 * j + 3]
     z = m[0]
     print(j, [x - z for x in c], [x - z for x in m], m[0] - t[5120 + 8 * (j - 1)])
