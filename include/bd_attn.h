@@ -139,7 +139,10 @@ int bd_dipo_group_stats(int32_t n_traj, const float* rewards, const int32_t* gro
 
 /* DiPO, step 2: token-level objective of Eq. 8 with the
  * stop-gradient behaviour policy of Eq. 7.
- *   logp, logp_old fp32 [n_tokens]    rho_k = exp(logp_k - logp_old_k)
+ *   logp, logp_old fp32 [n_tokens]    rho_k = exp(logp_k - logp_old_k); both NULL means
+ *                                      the online setting of Eq. 7 (pi_old = sg(pi_theta)):
+ *                                      rho == 1, so the weights are known before the
+ *                                      log-probs (enables the fused bd_logprob pass)
  *   traj_of_token  int32 [n_tokens]    local trajectory index
  *   rewards, group_of_traj             as in step 1 (local trajectories)
  *   group_stats    fp64 [n_groups, 3]  globally reduced output of step 1

@@ -39,7 +39,8 @@ __global__ void __launch_bounds__(256) token_loss_kernel(int64_t n, const float*
     const double mean_r = stats[3 * g + 0] / stats[3 * g + 1];
     const double A = (double)rewards[i] - mean_r;
     const double Ng = stats[3 * g + 2];
-    const double rho = exp((double)logp[k] - (double)logp_old[k]);
+    // logp == NULL: behaviour policy = sg(current policy) (Eq. 7), rho == 1
+    const double rho = logp ? exp((double)logp[k] - (double)logp_old[k]) : 1.0;
     const double lo = 1.0 - eps, hi = 1.0 + eps;
     const double rc = rho < lo ? lo : (rho > hi ? hi : rho);
     const double un = rho * A, cl = rc * A;
@@ -96,7 +97,7 @@ extern "C" int bd_dipo_token_loss(int64_t n_tokens, const float* logp, const flo
   using namespace bd;
   if (n_tokens < 0 || n_groups_global <= 0 || !(eps >= 0.f)) return set_error(BD_ERR_INVALID_ARG, "bad sizes");
   if (n_tokens == 0) return BD_OK;
-  if (!logp || !logp_old || !traj_of_token || !rewards || !group_of_traj || !group_stats || !dlogp || !partials)
+  if ((!logp) != (!logp_old) || !traj_of_token || !rewards || !group_of_traj || !group_stats || !dlogp || !partials)
     return set_error(BD_ERR_INVALID_ARG, "null pointer");
   long long blocks = (n_tokens + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;

@@ -1,9 +1,13 @@
 // bd_logprob: per-token log-softmax gather over the vocabulary, optionally
 // fused with its gradient (P:150-156 numerators of Eqs. 6-8; P:78 CE of Eq. 3;
-// S:69-77).  HBM-streaming: one CTA per row.
-//   pass 1: online (max, sum-exp) over the row in fp32 -> LSE_n; logp_n = z[t] - LSE_n
-//   pass 2 (dlogp given): dz[v] = w_n (1[v = t_n] - exp(z[v] - LSE_n)), re-reading
-//           the row (L2-resident: it was just streamed by pass 1).
+// S:69-77).  HBM-streaming.
+//  * forward only: one CTA per row, online (max, sum-exp) in fp32 -> LSE_n,
+//    logp_n = z[t] - LSE_n (one read of the logits).
+//  * forward + gradient (dlogp given, the online DiPO setting where the
+//    weights are known up front): a 4-CTA cluster per row keeps the row in
+//    shared memory (DSMEM max / sum exchange), one exp2 per element, one read
+//    and one write of the logits (logprob_fused_kernel); a generic two-pass
+//    path covers unaligned rows / vocabularies.
 // Rows are read with 16-byte vector loads when the row is 16-byte aligned and
 // V % 8 == 0 (Qwen3 V = 151,936 is), otherwise element-wise.
 #include "abi_common.h"
@@ -208,6 +212,147 @@ __global__ void __launch_bounds__(kThreads) logprob_bwd_kernel(int64_t n_rows, i
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused forward + gradient with the row held on chip: a cluster of kCl CTAs
+// per row, CTA c bulk-loads elements [c V/kCl, (c+1) V/kCl) into shared memory,
+// computes its (max, sum 2^(x - max)) partial, the partials are exchanged over
+// DSMEM, and the gradient is written from shared memory -- one HBM read and
+// one HBM write of the logits (the two-kernel path reads them twice).
+// Requires V % (8 kCl) == 0 and 16-byte aligned rows (Qwen3 V = 151,936 is).
+constexpr int kCl = 4;
+constexpr int kFusedThreads = 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float ld_dsmem_f32(const float* local, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ float block_reduce(float v, float* sh, bool is_max) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const float o = __shfl_xor_sync(0xffffffffu, v, off);
+    v = is_max ? fmaxf(v, o) : v + o;
+  }
+  if ((tid & 31) == 0) sh[tid >> 5] = v;
+  __syncthreads();
+  v = sh[0];
+  for (int w = 1; w < kFusedThreads / 32; ++w) v = is_max ? fmaxf(v, sh[w]) : v + sh[w];
+  __syncthreads();
+  return v;
+}
+
+// One exp2 per element: pass 1 row max (cluster-reduced over DSMEM), pass 2
+// e = 2^(x log2e - m) written back over the slice as bf16 plus the sum
+// (cluster-reduced), pass 3 dz = w (1[v = t] - e 2^(m - lse2)) from smem.
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
+    logprob_fused_kernel(int V, const __nv_bfloat16* z, int64_t stride, const int32_t* __restrict__ targets,
+                         float* __restrict__ logp, float* __restrict__ lse_out, const float* __restrict__ dlogp,
+                         __nv_bfloat16* dz, int64_t dz_stride) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ float red[kFusedThreads / 32];
+  __shared__ float part[2];  // [0] max, [1] sum of this CTA's slice
+  __shared__ float zt;       // target logit (if in this slice)
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t row = blockIdx.x / kCl;
+  const uint32_t crank = cluster_rank();
+  const int tid = threadIdx.x;
+  const int Vc = V / kCl;  // elements held by this CTA
+  const __nv_bfloat16* src = z + row * stride + (int64_t)crank * Vc;
+  uint4* buf4 = reinterpret_cast<uint4*>(smem);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t bytes = (uint32_t)Vc * 2;
+    mbar_expect_tx(&bar, bytes);
+    for (uint32_t off = 0; off < bytes; off += 32768) {
+      const uint32_t n = bytes - off < 32768 ? bytes - off : 32768;
+      bulk_load(smem + off, reinterpret_cast<const uint8_t*>(src) + off, n, &bar);
+    }
+  }
+  const int t = targets[row];
+  const int tl = t - (int)crank * Vc;  // target within this slice (may fall outside)
+  mbar_wait(&bar, 0);
+  if (tid == 0 && tl >= 0 && tl < Vc) zt = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(smem)[tl]);
+  // pass 1: max of the slice
+  const int nv = Vc / 8;
+  float mx = -INFINITY;
+  for (int i = tid; i < nv; i += kFusedThreads) {
+    const uint4 u = buf4[i];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      mx = fmaxf(mx, fmaxf(__uint_as_float(w[j] << 16), __uint_as_float(w[j] & 0xFFFF0000u)));
+  }
+  mx = block_reduce(mx, red, true);
+  if (tid == 0) part[0] = mx;
+  cluster_sync_all();
+  float m = -INFINITY;
+  for (uint32_t r = 0; r < (uint32_t)kCl; ++r) m = fmaxf(m, ld_dsmem_f32(&part[0], r));
+  const float m2 = m * kLog2e;
+  // pass 2: e = 2^(x log2e - m2) stored over the slice (bf16), partial sum
+  float sum = 0.f;
+  for (int i = tid; i < nv; i += kFusedThreads) {
+    const uint4 u = buf4[i];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float e0 = ex2_approx(fmaf(__uint_as_float(w[j] << 16), kLog2e, -m2));
+      const float e1 = ex2_approx(fmaf(__uint_as_float(w[j] & 0xFFFF0000u), kLog2e, -m2));
+      sum += e0 + e1;
+      o[j] = pack_bf16x2(e0, e1);
+    }
+    buf4[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  sum = block_reduce(sum, red, false);
+  if (tid == 0) part[1] = sum;
+  cluster_sync_all();
+  float tot = 0.f;
+  for (uint32_t r = 0; r < (uint32_t)kCl; ++r) tot += ld_dsmem_f32(&part[1], r);
+  const float lse = m + __logf(tot);
+  if (tid == 0) {
+    if (crank == 0) {
+      if (lse_out) lse_out[row] = lse;
+      if (t < 0 || t >= V) logp[row] = __int_as_float(0x7fc00000);
+    }
+    if (tl >= 0 && tl < Vc) logp[row] = zt - lse;
+  }
+  cluster_sync_all();  // peers' DSMEM reads of `part` complete before any CTA exits
+  if (!dlogp) return;
+  // pass 3: dz = w (1[v = t] - e / sum)
+  const float wgt = dlogp[row];
+  const float scl = wgt / tot;
+  uint4* out = reinterpret_cast<uint4*>(dz + row * dz_stride + (int64_t)crank * Vc);
+  for (int i = tid; i < nv; i += kFusedThreads) {
+    const uint4 u = buf4[i];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int v0 = 8 * i + 2 * j;
+      const float g0 = (v0 == tl ? wgt : 0.f) - scl * __uint_as_float(w[j] << 16);
+      const float g1 = (v0 + 1 == tl ? wgt : 0.f) - scl * __uint_as_float(w[j] & 0xFFFF0000u);
+      o[j] = pack_bf16x2(g0, g1);
+    }
+    out[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 }  // namespace
 }  // namespace bd
 
@@ -242,6 +387,24 @@ extern "C" int bd_logprob(int64_t n_rows, int32_t vocab, const void* logits, int
     return set_error(BD_ERR_INVALID_ARG, "in-place gradient needs equal strides");
   if (n_rows > 0x7FFFFFFF) return set_error(BD_ERR_UNSUPPORTED, "too many rows");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const bool fusable = dlogp && vocab % (8 * kCl) == 0 && row_stride % 8 == 0 && dlogits_stride % 8 == 0 &&
+                       aligned16(logits) && aligned16(dlogits) && (int64_t)n_rows * kCl <= 0x7FFFFFFF;
+  if (fusable) {
+    // one HBM read + one HBM write: the row stays in the cluster's shared memory
+    const int smem = vocab / kCl * 2;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(logprob_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(logprob_fused)");
+      attr = true;
+    }
+    if (smem > 200 * 1024) return set_error(BD_ERR_UNSUPPORTED, "vocab too large for the fused path");
+    logprob_fused_kernel<<<(unsigned)(n_rows * kCl), kFusedThreads, smem, stream>>>(
+        vocab, reinterpret_cast<const __nv_bfloat16*>(logits), row_stride, targets, logp, lse, dlogp,
+        reinterpret_cast<__nv_bfloat16*>(dlogits), dlogits_stride);
+    note_launches(1);
+    return check_cuda(cudaGetLastError(), "logprob_fused_kernel launch");
+  }
   logprob_kernel<<<(unsigned)n_rows, kThreads, 0, stream>>>(
       n_rows, vocab, reinterpret_cast<const __nv_bfloat16*>(logits), row_stride, targets, logp, lse, dlogp,
       reinterpret_cast<__nv_bfloat16*>(dlogits), dlogits_stride);

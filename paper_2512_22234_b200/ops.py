@@ -243,11 +243,15 @@ def dipo_token_loss(logp, logp_old, traj_of_token, rewards, group_of_traj, group
                     eps=0.2, partials=None):
     """bd_dipo_token_loss: returns (dlogp fp32 [n], partials fp64 [3] += (loss, tokens, clipped))."""
     _need_cuda(logp, logp_old, traj_of_token, rewards, group_of_traj, group_stats)
-    dlogp = torch.empty_like(logp)
+    if (logp is None) != (logp_old is None):
+        raise _lib.BdError("logp and logp_old must both be given or both be None (rho == 1)")
+    dlogp = torch.empty(traj_of_token.numel(), dtype=torch.float32, device=traj_of_token.device)
     if partials is None:
-        partials = torch.zeros(3, dtype=torch.float64, device=logp.device)
-    check(_lib.lib().bd_dipo_token_loss(logp.numel(), logp.data_ptr(), logp_old.data_ptr(), traj_of_token.data_ptr(),
+        partials = torch.zeros(3, dtype=torch.float64, device=traj_of_token.device)
+    lp = logp.data_ptr() if logp is not None else None
+    lo = logp_old.data_ptr() if logp_old is not None else None
+    check(_lib.lib().bd_dipo_token_loss(traj_of_token.numel(), lp, lo, traj_of_token.data_ptr(),
                                         rewards.data_ptr(), group_of_traj.data_ptr(), group_stats.data_ptr(),
                                         int(n_groups_global), float(eps), dlogp.data_ptr(), partials.data_ptr(),
-                                        _stream_ptr(logp)), "bd_dipo_token_loss")
+                                        _stream_ptr(traj_of_token)), "bd_dipo_token_loss")
     return dlogp, partials

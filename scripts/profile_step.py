@@ -23,5 +23,6 @@ dq, dk, dv = bd.attn_bwd(prob, q, k, v, o, lse, do)
 z, t = logits_inputs(2048, 151936, device="cuda")
 logp, lz = ops.logprob(z, t)
 ops.logprob_bwd(z, t, lz, torch.ones_like(logp), dlogits=z)
+ops.logprob(z, t, dlogp=torch.ones_like(logp), dlogits=z)  # cluster-fused path
 torch.cuda.synchronize()
 print("done", name, batch)
