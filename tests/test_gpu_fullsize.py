@@ -20,7 +20,7 @@ import torch
 import paper_2512_22234_b200 as bd
 from paper_2512_22234_b200 import ops
 from oracle import Problem as OProblem, attention, mask, logprob as olp
-from parity import FWD_MAX_ABS, FWD_REL_L2, GRAD_REL_L2, LOGP_MAX_ABS, metrics, t2np
+from parity import FWD_MAX_ABS, FWD_REL_L2, GRAD_REL_L2, LOGP_MAX_ABS, DZ_REL_L2, metrics, t2np
 from workloads import CONFIGS, attn_inputs, logits_inputs, VOCAB_QWEN3
 
 
@@ -115,3 +115,12 @@ def test_fullsize_logprob_sampled(cuda_ok):
     m = metrics(t2np(logp[rows]), ref_lp)
     assert m["finite"] and m["max_abs"] <= LOGP_MAX_ABS, m
     assert metrics(t2np(lse[rows]), ref_lse)["max_abs"] <= LOGP_MAX_ABS
+    # the cluster-fused forward + gradient, in place, as bench.py launches it
+    z_rows = z[rows].float().cpu()
+    w = torch.linspace(-2, 2, n, device="cuda")
+    logp2, lse2, _ = ops.logprob(z, t, dlogp=w, dlogits=z)
+    torch.cuda.synchronize()
+    assert metrics(t2np(logp2[rows]), ref_lp)["max_abs"] <= LOGP_MAX_ABS
+    ref_dz = olp.logprob_grad(z_rows, t[rows].long().cpu(), t2np(w[rows]).astype(np.float64))
+    md = metrics(t2np(z[rows]), ref_dz)
+    assert md["finite"] and md["rel_l2"] <= DZ_REL_L2, md
