@@ -41,7 +41,7 @@ def _slice(x, b, h):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["sdar_1_7b", "sdar_8b"])
+@pytest.mark.parametrize("name", ["sdar_1_7b", "sdar_8b", "sweep_b8", "sweep_b32"])
 def test_fullsize_sampled_parity(cuda_ok, name):
     cfg = CONFIGS[name]
     prob = bd.Problem.from_cfg(cfg)
