@@ -15,11 +15,15 @@ Sources:
 * DiRL repeats prompt and response blockwise (P:261, Fig. 4b);
   TraceRL repeats only the output (Fig. 4a) -> ``repeat_prompt``.
 
+* Trace replay (reading c19, Eq. 6): with S noisy
+  copies, copy s of block k is one conditioning state; it "sees CLEAN earlier
+  blocks and itself" -- never another copy.
+
 Rule table (query segment, key segment -> visible iff):
-    x0 -> x0 : blk(pk) <= blk(pq)
-    xt -> x0 : blk(pk) <  blk(pq)
-    xt -> xt : blk(pk) == blk(pq)
-    x0 -> xt : never
+    x0    -> x0    : blk(pk) <= blk(pq)
+    xt(s) -> x0    : blk(pk) <  blk(pq)
+    xt(s) -> xt(u) : s == u and blk(pk) == blk(pq)
+    x0    -> xt    : never
 
 ORACLE: test infrastructure only (see oracle/__init__.py).
 """
@@ -29,31 +33,42 @@ import numpy as np
 from .problem import Problem
 
 
-def packed_segments(prob: Problem):
-    """Return (is_noisy[Ntot] bool, clean_pos[Ntot] int64) for the packed axis.
+def packed_copies(prob: Problem):
+    """Return (copy[Ntot] int64, clean_pos[Ntot] int64) for the packed axis.
 
-    Packed index n < L is x0 at clean position n; n >= L is xt at clean
-    position xb + (n - L) (reading c1: concatenated [x0 | xt]; noisy copies
-    keep their source positions, S:139 / S:169)."""
-    L, xb, N = prob.L, prob.xb, prob.ntot
+    Packed index n < L is x0 (copy 0) at clean position n; the noisy copies
+    follow, copy s (1..S) occupying [L + (s-1)(L-xb), L + s(L-xb)) at clean
+    positions xb.. L-1 (reading c1: concatenated [x0 | xt^(1) | ...]; noisy
+    copies keep their source positions, S:139 / S:169)."""
+    L, xb, N, Ln = prob.L, prob.xb, prob.ntot, prob.n_noisy
     n = np.arange(N, dtype=np.int64)
     noisy = n >= L
-    pos = np.where(noisy, xb + (n - L), n)
-    return noisy, pos
+    j = np.where(noisy, n - L, 0)
+    copy = np.where(noisy, 1 + j // max(Ln, 1), 0)
+    pos = np.where(noisy, xb + j % max(Ln, 1), n)
+    return copy, pos
+
+
+def packed_segments(prob: Problem):
+    """Return (is_noisy[Ntot] bool, clean_pos[Ntot] int64)."""
+    copy, pos = packed_copies(prob)
+    return copy > 0, pos
 
 
 def mask_rows(prob: Problem, rows) -> np.ndarray:
     """Visibility M[rows, :] (bool) straight from the rule table."""
-    noisy, pos = packed_segments(prob)
+    copy, pos = packed_copies(prob)
+    noisy = copy > 0
     rows = np.asarray(rows, dtype=np.int64)
     B = prob.block_size
     bq = (pos[rows] // B)[:, None]
     bk = (pos // B)[None, :]
     q_noisy = noisy[rows][:, None]
     k_noisy = noisy[None, :]
+    same_copy = copy[rows][:, None] == copy[None, :]
     clean_clean = (~q_noisy) & (~k_noisy) & (bk <= bq)
     noisy_clean = q_noisy & (~k_noisy) & (bk < bq)
-    noisy_noisy = q_noisy & k_noisy & (bk == bq)
+    noisy_noisy = q_noisy & k_noisy & same_copy & (bk == bq)
     return clean_clean | noisy_clean | noisy_noisy
 
 

@@ -12,6 +12,14 @@ xb..L-1, with xb = 0 when the prompt is repeated too (DiRL, Fig. 4b,
 ``repeat_prompt=1``) and xb = P when only the response is repeated
 (TraceRL, Fig. 4a, ``repeat_prompt=0``).
 
+Trace replay (reading c19): Eq. 6
+conditions every decoded token o_k in tau_i(t) on the prefix tau_i(1:t-1),
+the block's state *before* decoding step t.  With S decoding steps per block
+(static decoding, B/S tokens per step) the packed axis becomes
+[x0 | xt^(1) | ... | xt^(S)]: copy s holds every block's state before step s
+("one NOISY copy of that block holding the block's state BEFORE
+step t").  ``n_copies`` = S; S = 1 is the single-copy DiRL layout.
+
 This module is part of the oracle and deliberately independent of the
 package's own problem struct.
 """
@@ -31,6 +39,7 @@ class Problem:
     head_dim: int
     repeat_prompt: int = 1
     softmax_scale: float = 0.0  # <= 0 -> 1/sqrt(head_dim)  ("qk^T/sqrt(d)")
+    n_copies: int = 1           # S noisy copies (trace replay, reading c19)
 
     @property
     def L(self) -> int:
@@ -48,8 +57,8 @@ class Problem:
 
     @property
     def ntot(self) -> int:
-        """Packed length: 2L (DiRL) or 2L - P (response-only)."""
-        return self.L + self.n_noisy
+        """Packed length: L + S (L - xb); 2L (DiRL) or 2L - P (response-only) at S = 1."""
+        return self.L + self.n_copies * self.n_noisy
 
     @property
     def scale(self) -> float:
@@ -64,6 +73,8 @@ class Problem:
             raise ValueError("non-positive dimension")
         if self.prompt_len < 0 or self.response_len < 0 or self.L <= 0:
             raise ValueError("bad lengths")
+        if self.n_copies < 1:
+            raise ValueError("n_copies < 1")
         if self.n_q_heads % self.n_kv_heads:
             raise ValueError("n_q_heads % n_kv_heads != 0")
         # S:214 "length not multiple of B -> layout error" (reading c4)

@@ -2,8 +2,9 @@
 must equal bit-exactly).
 
 The packed axis of each segment is cut into 128-row tiles starting at the
-segment start: x0 tiles cover packed rows [128 j, min(128 j + 128, L)), xt
-tiles cover [L + 128 j, min(L + 128 j + 128, Ntot)).  For every (q-tile,
+segment start: x0 tiles cover packed rows [128 j, min(128 j + 128, L)), the
+tiles of noisy copy s cover [c_s + 128 j, min(c_s + 128 j + 128, c_s + L - xb))
+with c_s = L + (s-1)(L - xb).  For every (q-tile,
 k-tile) pair the kind is read off the dense mask restricted to the tile's
 valid rows/columns:
 
@@ -29,10 +30,12 @@ FULL, PARTIAL = 1, 2
 
 
 def segment_tiles(prob: Problem, tile: int = 128):
-    """[(seg, tile_idx, start, end)] over both segments in packed order."""
+    """[(seg, tile_idx, start, end)] over all segments in packed order
+    (seg 0 = x0, seg s = noisy copy s; each segment tiled from its start)."""
     out = []
-    L, N = prob.L, prob.ntot
-    for seg, (s0, s1) in enumerate(((0, L), (L, N))):
+    L, Ln = prob.L, prob.n_noisy
+    bounds = [(0, L)] + [(L + (s - 1) * Ln, L + s * Ln) for s in range(1, prob.n_copies + 1)]
+    for seg, (s0, s1) in enumerate(bounds):
         j = 0
         for a in range(s0, s1, tile):
             out.append((seg, j, a, min(a + tile, s1)))

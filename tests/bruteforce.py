@@ -13,11 +13,15 @@ Pure Python loops -- only for small cases.
 """
 
 
-def visibility_sets(L, P, B, repeat_prompt):
+def visibility_sets(L, P, B, repeat_prompt, n_copies=1):
     """Return (tokens, vis) where tokens[n] = (segment, clean_pos) in packed
-    order [x0 | xt] and vis[n] is the set of visible packed indices."""
+    order [x0 | xt^(1) | ... | xt^(S)] and vis[n] is the set of visible packed
+    indices.  Trace replay (S copies): copy s of block k is its own
+    conditioning state -- it sees the clean blocks < k and itself only."""
     xb = 0 if repeat_prompt else P
-    tokens = [("x0", p) for p in range(L)] + [("xt", p) for p in range(xb, L)]
+    tokens = [("x0", p) for p in range(L)]
+    for c in range(1, n_copies + 1):
+        tokens += [("xt%d" % c, p) for p in range(xb, L)]
     # group packed indices by (segment, block)
     blocks = {}
     for n, (seg, p) in enumerate(tokens):
@@ -33,7 +37,7 @@ def visibility_sets(L, P, B, repeat_prompt):
         else:
             for kk in range(0, k):
                 s |= blocks.get(("x0", kk), set())
-            s |= blocks.get(("xt", k), set())
+            s |= blocks.get((seg, k), set())
         assert k < n_blocks
         vis.append(s)
     return tokens, vis
