@@ -5,9 +5,10 @@
 
 A STEP is one pass of the whole hot path over one batch of
 synthetic, device-resident inputs, per rank:
-    bd_attn_fwd (tile map a1 + a2) -> bd_logprob (a6) -> DiPO group stats +
-    token loss + NCCL all-reduce of the scalar partials (a7) -> bd_logprob_bwd
-    (a8, in place) -> bd_attn_bwd (a3-a5, tile map rebuilt on device).
+    bd_attn_fwd (tile map a1 + a2) -> DiPO group stats + token weights + NCCL
+    all-reduce of the scalar partials (a7; online update, rho == 1, Eq. 7) ->
+    bd_logprob forward + gradient fused in one pass, in place (a6 + a8) ->
+    bd_attn_bwd (a3-a5, tile map rebuilt on device).
 The transformer between attention and the logits is the caller's (out of
 scope): the logits are a resident synthetic stand-in for the LM-head output at
 the response positions (N = b R rows x V = 151,936).
@@ -16,7 +17,8 @@ Metric (BASELINE.json): bd-attn fwd+bwd useful TFLOP/s (& % BF16 peak) and
 train tokens/s.  `value` = useful attention FLOPs of the step summed over all
 ranks / step time (max over ranks), i.e. the whole step's time including
 logprob and DiPO.  Useful FLOPs count only visible (query, key) pairs:
-fwd = 4 d Hq b pairs, bwd = 2.5 fwd, pairs = L (L + B).
+fwd = 4 d Hq b pairs, bwd = 2.5 fwd, pairs = L (L + B), or
+(1 + S) L (L + B) / 2 for the trace-replay config with S noisy copies.
 Multi-GPU: one process per GPU (torchrun), each rank runs its own GRPO
 group(s) of sequences -> weak scaling; NCCL only all-reduces DiPO scalars.
 """
@@ -319,7 +321,7 @@ def run_ours(args):
         "config": {"workload": cfg.name, "batch_per_gpu": cfg.batch, "global_batch": cfg.batch * world,
                    "n_q_heads": cfg.n_q_heads, "n_kv_heads": cfg.n_kv_heads, "head_dim": cfg.head_dim,
                    "prompt_len": cfg.prompt_len, "response_len": cfg.response_len, "block_size": cfg.block_size,
-                   "packed_len": cfg.ntot, "vocab": step.V, "logprob_rows_per_gpu": step.n_rows,
+                   "packed_len": cfg.ntot, "n_copies": cfg.n_copies, "vocab": step.V, "logprob_rows_per_gpu": step.n_rows,
                    "parallelism": f"dp{world} (sequence-sharded, one GRPO group per rank)",
                    "l2": "inputs larger than L2 (q alone %.1f GB >> 126 MB)" % (step.q.numel() * 2 / 1e9)},
         "pct_bf16_peak": round(value / world / peak_s * 100, 2),
@@ -369,7 +371,8 @@ def oracle_sample(cfg, n_rows, seed=0):
     packed length.  Returns (seconds, useful_flops, description)."""
     import numpy as np
     from oracle import Problem as OP, attention, mask
-    prob = OP(1, cfg.prompt_len, cfg.response_len, cfg.block_size, 1, 1, cfg.head_dim, cfg.repeat_prompt)
+    prob = OP(1, cfg.prompt_len, cfg.response_len, cfg.block_size, 1, 1, cfg.head_dim, cfg.repeat_prompt,
+              n_copies=cfg.n_copies)
     g = torch.Generator().manual_seed(seed)
     N, d = prob.ntot, prob.head_dim
     q = torch.randn((1, N, 1, d), generator=g).to(torch.bfloat16)

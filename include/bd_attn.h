@@ -72,6 +72,12 @@ typedef struct bd_problem {
   int32_t head_dim;      /* d in {64, 128}                             */
   int32_t repeat_prompt; /* 1 = DiRL (default), 0 = response-only       */
   float softmax_scale;   /* <= 0 -> 1/sqrt(head_dim)            */
+  int32_t n_copies;      /* S noisy copies, 0 or 1 = single copy; S > 1 =
+                          * trace replay (Eq. 6):
+                          * packed [x0 | xt(1) | ... | xt(S)], copy s = every
+                          * block's state before decoding step s; copy s of
+                          * block k sees x0 blocks < k and itself only
+                          * (reading c19)                      */
 } bd_problem;
 
 /* Packed length Ntot of one sequence, or -1 if the problem is invalid. */

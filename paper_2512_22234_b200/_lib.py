@@ -24,6 +24,7 @@ class BdProblem(ctypes.Structure):
         ("head_dim", ctypes.c_int32),
         ("repeat_prompt", ctypes.c_int32),
         ("softmax_scale", ctypes.c_float),
+        ("n_copies", ctypes.c_int32),
     ]
 
 

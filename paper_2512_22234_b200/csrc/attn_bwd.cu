@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
 #pragma unroll
   for (int off = kTpr / 2; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if (n < N && sub == 0) {
-    const int t = n >= g.L ? g.T0 + (n - g.L) / kTileRows : n / kTileRows;
+    const int t = tile_of_row(g, n);
     const int r = n - tile_start(g, t);
     const size_t slot = ((size_t)bh * g.NT + t) * kTileRows + r;
     dsum_t[slot] = acc;
@@ -232,7 +232,8 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
   const int n_qt = mv.col_ptr()[kt + 1] - e0;
   const int* ents = mv.col_ent() + e0;
   const int n_it = n_qt * a.group;
-  const int k0 = tile_start(g, kt), k1 = tile_end(g, kt), kseg = tile_seg(g, kt);
+  int k0, k1, kseg;
+  tile_bounds(g, kt, k0, k1, kseg);
   auto slot_of = [](int idx) { return idx % C::kSlots; };
   auto phase_of = [](int idx) { return (uint32_t)((idx / C::kSlots) & 1); };
 
@@ -380,7 +381,8 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
     for (int i = 0; i < n_it; ++i) {
       const int ent = ents[n_qt - 1 - i / a.group];
       const int qt = entry_tile(ent);
-      const int q0 = tile_start(g, qt), q1 = tile_end(g, qt), qseg = tile_seg(g, qt);
+      int q0, q1, qseg;
+      tile_bounds(g, qt, q0, q1, qseg);
       const bool need_mask = entry_kind(ent) == kKindPartial || (q1 - q0) < 128 || (k1 - k0) < 128;
       const float* sv = reinterpret_cast<const float*>(smem + C::kOffVec + (i & 1) * C::kVecBytes) + wg * NC;
       mbar_wait(&vec_full[i & 1], (i >> 1) & 1);
@@ -559,7 +561,8 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
   const int e0 = mv.row_ptr()[qt];
   const int n_kt = mv.row_ptr()[qt + 1] - e0;
   const int* ents = mv.row_ent() + e0;
-  const int q0 = tile_start(g, qt), q1 = tile_end(g, qt), qseg = tile_seg(g, qt);
+  int q0, q1, qseg;
+  tile_bounds(g, qt, q0, q1, qseg);
 
   if (warp == 0) tmem_alloc<C::kTmemCols>(tslot);
   if (warp == C::kTmaWarp && lane == 0) {
@@ -688,7 +691,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
     const int row = q0 + r;
     int lo0, hi0, lo1, hi1;
     row_interval(g, qseg, row, 0, lo0, hi0);
-    row_interval(g, qseg, row, 1, lo1, hi1);
+    row_interval(g, qseg, row, qseg ? qseg : 1, lo1, hi1);  // the row's own noisy copy
     const size_t vslot = (((size_t)b * a.n_q_heads + h) * g.NT + qt) * kTileRows + r;
     const float lse2 = a.lse2_t[vslot];
     const float dsum = a.dsum_t[vslot];

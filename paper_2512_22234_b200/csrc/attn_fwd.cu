@@ -148,7 +148,8 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
   const int e0 = mv.row_ptr()[qt];
   const int n_kt = mv.row_ptr()[qt + 1] - e0;
   const int* ents = mv.row_ent() + e0;
-  const int q0 = tile_start(g, qt), q1 = tile_end(g, qt), qseg = tile_seg(g, qt);
+  int q0, q1, qseg;
+  tile_bounds(g, qt, q0, q1, qseg);
 
   if (warp == 0) tmem_alloc<C::kTmemCols>(tslot);
   if (warp == C::kTmaWarp && lane == 0) {
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
     const int row = q0 + r;
     int lo0, hi0, lo1, hi1;
     row_interval(g, qseg, row, 0, lo0, hi0);
-    row_interval(g, qseg, row, 1, lo1, hi1);
+    row_interval(g, qseg, row, qseg ? qseg : 1, lo1, hi1);  // the row's own noisy copy
     const float sl2 = a.scale_log2;
     float m = -INFINITY, l = 0.f;
 

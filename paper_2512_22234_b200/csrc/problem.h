@@ -22,15 +22,19 @@ inline int validate_problem(const bd_problem* p) {
   if (L % p->block_size) return set_error(BD_ERR_LAYOUT, "L = %lld not a multiple of block_size %d", (long long)L,
                                           p->block_size);
   if (p->repeat_prompt != 0 && p->repeat_prompt != 1) return set_error(BD_ERR_INVALID_ARG, "repeat_prompt not 0/1");
-  if (2 * L > (int64_t)1 << 30) return set_error(BD_ERR_UNSUPPORTED, "sequence too long");
-  const int T = (int)((L + kTileRows - 1) / kTileRows);
-  if (2 * T > kMaxTiles) return set_error(BD_ERR_UNSUPPORTED, "sequence too long for the tile map");
+  if (p->n_copies < 0) return set_error(BD_ERR_INVALID_ARG, "n_copies < 0");
+  const int64_t S = p->n_copies > 1 ? p->n_copies : 1;
+  const int64_t Lx = L - (p->repeat_prompt ? 0 : p->prompt_len);
+  if (L + S * Lx > (int64_t)1 << 30) return set_error(BD_ERR_UNSUPPORTED, "sequence too long");
+  const int64_t NT = (L + kTileRows - 1) / kTileRows + S * ((Lx + kTileRows - 1) / kTileRows);
+  if (NT > kMaxTiles) return set_error(BD_ERR_UNSUPPORTED, "sequence too long for the tile map (%lld tiles)",
+                                       (long long)NT);
   return BD_OK;
 }
 
 inline Geom geom_of(const bd_problem& p) {
   const int L = p.prompt_len + p.response_len;
-  return make_geom(L, p.repeat_prompt ? 0 : p.prompt_len, p.block_size);
+  return make_geom(L, p.repeat_prompt ? 0 : p.prompt_len, p.block_size, p.n_copies);
 }
 
 inline float scale_of(const bd_problem& p) {

@@ -31,59 +31,102 @@ constexpr int kKindPartial = 2;
 
 struct Geom {
   int L, xb, N, B, T0, T1, NT;
+  int S;   // noisy copies (trace replay, reading c19); 1 = DiRL single copy
+  int Lx;  // L - xb: length of one noisy copy
 };
 
-__host__ __device__ inline Geom make_geom(int L, int xb, int B) {
+__host__ __device__ inline Geom make_geom(int L, int xb, int B, int S = 1) {
   Geom g;
   g.L = L;
   g.xb = xb;
-  g.N = L + (L - xb);
+  g.S = S < 1 ? 1 : S;
+  g.Lx = L - xb;
+  g.N = L + g.S * g.Lx;
   g.B = B;
   g.T0 = (L + kTileRows - 1) / kTileRows;
-  g.T1 = (L - xb + kTileRows - 1) / kTileRows;
-  g.NT = g.T0 + g.T1;
+  g.T1 = (g.Lx + kTileRows - 1) / kTileRows;
+  g.NT = g.T0 + g.S * g.T1;
   return g;
 }
 
-__host__ __device__ inline int tile_seg(const Geom& g, int t) { return t >= g.T0 ? 1 : 0; }
-__host__ __device__ inline int tile_idx(const Geom& g, int t) { return t >= g.T0 ? t - g.T0 : t; }
+// Segments: 0 = x0 (packed [0, L)), s = 1..S noisy copy s (packed
+// [L + (s-1) Lx, L + s Lx)).  Each segment is tiled from its own start.
+__host__ __device__ inline int seg_base(const Geom& g, int s) { return s ? g.L + (s - 1) * g.Lx : 0; }
+__host__ __device__ inline int seg_end(const Geom& g, int s) { return s ? g.L + s * g.Lx : g.L; }
+// (S == 1, the hot path, avoids the integer divisions: the kernels evaluate
+// these per tile in their inner loops.)
+__host__ __device__ inline int seg_of_row(const Geom& g, int n) {
+  return n < g.L ? 0 : (g.S == 1 ? 1 : 1 + (n - g.L) / g.Lx);
+}
+__host__ __device__ inline int seg_first_tile(const Geom& g, int s) { return s ? g.T0 + (s - 1) * g.T1 : 0; }
+__host__ __device__ inline int tile_seg(const Geom& g, int t) {
+  return t < g.T0 ? 0 : (g.S == 1 ? 1 : 1 + (t - g.T0) / g.T1);
+}
+__host__ __device__ inline int tile_idx(const Geom& g, int t) {
+  return t < g.T0 ? t : (g.S == 1 ? t - g.T0 : (t - g.T0) % g.T1);
+}
+// [start, end) and segment of tile t with at most one division
+__host__ __device__ inline void tile_bounds(const Geom& g, int t, int& start, int& end, int& seg) {
+  if (t < g.T0) {
+    seg = 0;
+    start = t * kTileRows;
+    end = start + kTileRows < g.L ? start + kTileRows : g.L;
+    return;
+  }
+  const int j = t - g.T0;
+  const int s = g.S == 1 ? 0 : j / g.T1;
+  const int base = g.L + s * g.Lx;
+  seg = s + 1;
+  start = base + (j - s * g.T1) * kTileRows;
+  end = start + kTileRows < base + g.Lx ? start + kTileRows : base + g.Lx;
+}
 __host__ __device__ inline int tile_start(const Geom& g, int t) {
-  return t >= g.T0 ? g.L + (t - g.T0) * kTileRows : t * kTileRows;
+  int a, b, s;
+  tile_bounds(g, t, a, b, s);
+  return a;
 }
 __host__ __device__ inline int tile_end(const Geom& g, int t) {
-  const int s = tile_start(g, t) + kTileRows;
-  const int e = t >= g.T0 ? g.N : g.L;
-  return s < e ? s : e;
+  int a, b, s;
+  tile_bounds(g, t, a, b, s);
+  return b;
+}
+// q-tile holding packed row n
+__host__ __device__ inline int tile_of_row(const Geom& g, int n) {
+  if (n < g.L) return n / kTileRows;
+  const int j = n - g.L, s = g.S == 1 ? 0 : j / g.Lx;
+  return g.T0 + s * g.T1 + (j - s * g.Lx) / kTileRows;
 }
 
 // Visible packed-column interval [lo, hi) of packed row `row` (a row of
 // segment `qseg`) within key segment `kseg`.  Empty intervals have lo >= hi.
+// A noisy row sees no other copy (reading c19), so for kseg >= 1 only
+// kseg == qseg is non-empty.
 __host__ __device__ inline void row_interval(const Geom& g, int qseg, int row, int kseg, int& lo, int& hi) {
-  const int p = qseg ? g.xb + (row - g.L) : row;  // clean position
+  const int p = qseg ? g.xb + (row - seg_base(g, qseg)) : row;  // clean position
   const int bq = p / g.B;
   const int b0 = bq * g.B, b1 = b0 + g.B;
   if (kseg == 0) {
     lo = 0;
     hi = qseg ? b0 : (b1 < g.L ? b1 : g.L);
-  } else if (qseg == 0) {
-    lo = hi = g.L;  // x0 never sees xt
+  } else if (qseg != kseg) {
+    lo = hi = seg_base(g, kseg);  // x0 never sees xt; copies never see each other
   } else {
     const int a = b0 > g.xb ? b0 : g.xb;
     const int c = b1 < g.L ? b1 : g.L;
-    lo = g.L + a - g.xb;
-    hi = g.L + c - g.xb;
+    lo = seg_base(g, kseg) + a - g.xb;
+    hi = seg_base(g, kseg) + c - g.xb;
   }
 }
 
 // The transpose view used by the backward's key-row threads: the packed query
 // rows of segment `qseg` that see key `key` (a packed row of segment kseg)
 // also form one interval [qa, qb) (row intervals are monotone in the row):
-//   x0 key, x0 rows:  blk(q) >= blk(k)      -> [blk(k) B, L)
-//   x0 key, xt rows:  blk(q) >= blk(k) + 1  -> clean positions >= (blk(k)+1) B
-//   xt key, xt rows:  blk(q) == blk(k)      -> its own block (clipped to xb)
-//   xt key, x0 rows:  never
+//   x0 key, x0 rows:        blk(q) >= blk(k)      -> [blk(k) B, L)
+//   x0 key, copy-s rows:    blk(q) >= blk(k) + 1  -> clean positions >= (blk(k)+1) B
+//   copy-s key, copy-s rows: blk(q) == blk(k)     -> its own block (clipped to xb)
+//   xt key, x0 rows / another copy's rows: never
 __host__ __device__ inline void key_interval(const Geom& g, int kseg, int key, int qseg, int& qa, int& qb) {
-  const int pk = kseg ? g.xb + (key - g.L) : key;
+  const int pk = kseg ? g.xb + (key - seg_base(g, kseg)) : key;
   const int bk = pk / g.B;
   if (qseg == 0) {
     if (kseg) {
@@ -92,6 +135,8 @@ __host__ __device__ inline void key_interval(const Geom& g, int kseg, int key, i
       qa = bk * g.B;
       qb = g.L;
     }
+  } else if (kseg && kseg != qseg) {
+    qa = qb = seg_base(g, qseg);
   } else {
     int a, b;  // clean positions
     if (kseg == 0) {
@@ -102,8 +147,8 @@ __host__ __device__ inline void key_interval(const Geom& g, int kseg, int key, i
       b = (bk + 1) * g.B < g.L ? (bk + 1) * g.B : g.L;
     }
     if (a < g.xb) a = g.xb;
-    qa = g.L + a - g.xb;
-    qb = g.L + b - g.xb;
+    qa = seg_base(g, qseg) + a - g.xb;
+    qb = seg_base(g, qseg) + b - g.xb;
     if (qb < qa) qb = qa;
   }
 }
@@ -126,17 +171,17 @@ __host__ __device__ inline int classify_pair(const Geom& g, int qt, int kt) {
 }
 
 // Candidate k-tiles of q-tile qt: the union of its rows' intervals is
-// [0, hi0) in x0 and [lo1, hi1) in xt (intervals are monotone and the xt ones
-// of consecutive blocks are adjacent), so only tiles overlapping those ranges
-// are classified.
+// [0, hi0) in x0 and [lo1, hi1) in its own copy (intervals are monotone and
+// the xt ones of consecutive blocks are adjacent), so only tiles overlapping
+// those ranges are classified.
 __host__ __device__ inline void candidate_range(const Geom& g, int qt, int kseg, int& t_lo, int& t_hi) {
   const int q0 = tile_start(g, qt), q1 = tile_end(g, qt), qs = tile_seg(g, qt);
   int lo_a, hi_a, lo_b, hi_b;
   row_interval(g, qs, q0, kseg, lo_a, hi_a);
   row_interval(g, qs, q1 - 1, kseg, lo_b, hi_b);
   const int lo = lo_a, hi = hi_b;
-  const int base = kseg ? g.T0 : 0;
-  const int seg0 = kseg ? g.L : 0;
+  const int base = seg_first_tile(g, kseg);
+  const int seg0 = seg_base(g, kseg);
   if (hi <= lo) {
     t_lo = t_hi = base;
     return;
@@ -173,7 +218,7 @@ struct MapView {
   __host__ __device__ int* bwd_order() const { return fwd_order() + NT; }
 };
 
-// Upper bound on entries: a q-tile lists at most T0 x0 tiles and 2 xt tiles
+// Upper bound on entries: a q-tile lists at most T0 x0 tiles and 2 tiles of its own copy
 // (its own block spans at most two xt tiles when B <= 128; in general
 // ceil(B/128)+1).
 __host__ __device__ inline int map_capacity(const Geom& g) {

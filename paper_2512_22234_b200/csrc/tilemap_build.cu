@@ -25,7 +25,9 @@ void build_map_host(const Geom& g, std::vector<int>& w) {
   std::vector<int> rowlen(g.NT), collen(g.NT, 0);
   for (int t = 0; t < g.NT; ++t) {
     mv.row_ptr()[t] = n;
-    for (int ks = 0; ks < 2; ++ks) {
+    const int qs = tile_seg(g, t);
+    for (int kk = 0; kk < (qs ? 2 : 1); ++kk) {
+      const int ks = kk ? qs : 0;  // x0, then the row's own copy
       int a, b;
       candidate_range(g, t, ks, a, b);
       for (int kt = a; kt < b; ++kt) {
@@ -134,15 +136,16 @@ __global__ void __launch_bounds__(kBuildThreads, 1) build_map_kernel(Geom g, int
       const int q0 = tile_start(g, t), nrow = tile_end(g, t) - q0, qs = tile_seg(g, t);
       for (int r = lane; r < nrow; r += 32) {
         row_interval(g, qs, q0 + r, 0, wiv[r], wiv[128 + r]);
-        row_interval(g, qs, q0 + r, 1, wiv[256 + r], wiv[384 + r]);
+        if (qs) row_interval(g, qs, q0 + r, qs, wiv[256 + r], wiv[384 + r]);
       }
       __syncwarp();
       int n = pass ? mv.row_ptr()[t] : 0;
-      for (int ks = 0; ks < 2; ++ks) {
+      for (int kk = 0; kk < (qs ? 2 : 1); ++kk) {
+        const int ks = kk ? qs : 0;  // x0, then the row's own copy
         int a, b;
         candidate_range(g, t, ks, a, b);
         for (int kt = a; kt < b; ++kt) {
-          const int kind = classify_pair_warp(g, t, kt, wiv + 256 * ks, wiv + 256 * ks + 128);
+          const int kind = classify_pair_warp(g, t, kt, wiv + 256 * kk, wiv + 256 * kk + 128);
           if (kind) {
             if (pass && lane == 0) {
               mv.row_ent()[n] = entry_make(kt, kind);
@@ -289,9 +292,9 @@ extern "C" int bd_tilemap_selfcheck(const bd_problem* prob, int64_t* mismatches)
   if ((int64_t)g.N * g.N > (int64_t)1 << 26) return set_error(BD_ERR_UNSUPPORTED, "problem too large for selfcheck");
   int64_t bad = 0;
   for (int r = 0; r < g.N; ++r) {
-    const int qs = r >= g.L ? 1 : 0;
+    const int qs = seg_of_row(g, r);
     for (int k = 0; k < g.N; ++k) {
-      const int ks = k >= g.L ? 1 : 0;
+      const int ks = seg_of_row(g, k);
       int lo, hi, qa, qb;
       row_interval(g, qs, r, ks, lo, hi);
       key_interval(g, ks, k, qs, qa, qb);

@@ -31,6 +31,7 @@ class Problem:
     head_dim: int
     repeat_prompt: int = 1
     softmax_scale: float = 0.0
+    n_copies: int = 1  # S noisy copies (trace replay, reading c19)
 
     @property
     def L(self):
@@ -42,7 +43,7 @@ class Problem:
 
     @property
     def ntot(self):
-        return 2 * self.L - self.xb
+        return self.L + max(self.n_copies, 1) * (self.L - self.xb)
 
     @property
     def scale(self):
@@ -50,7 +51,8 @@ class Problem:
 
     def c(self):
         return BdProblem(self.batch, self.prompt_len, self.response_len, self.block_size, self.n_q_heads,
-                         self.n_kv_heads, self.head_dim, self.repeat_prompt, float(self.softmax_scale))
+                         self.n_kv_heads, self.head_dim, self.repeat_prompt, float(self.softmax_scale),
+                         self.n_copies)
 
     def with_(self, **kw):
         return replace(self, **kw)
@@ -58,7 +60,7 @@ class Problem:
     @staticmethod
     def from_cfg(cfg, **kw):
         p = Problem(cfg.batch, cfg.prompt_len, cfg.response_len, cfg.block_size, cfg.n_q_heads,
-                    cfg.n_kv_heads, cfg.head_dim, cfg.repeat_prompt)
+                    cfg.n_kv_heads, cfg.head_dim, cfg.repeat_prompt, n_copies=getattr(cfg, "n_copies", 1))
         return p.with_(**kw) if kw else p
 
 

@@ -20,12 +20,17 @@ CASES = [
     ("B32_d64_gqa2", AttnConfig("c7", 1, 4, 2, 64, 96, 416, 32)),
     ("tiny_L_lt_tile", AttnConfig("c8", 1, 2, 1, 128, 8, 24, 8)),
     ("big_block_B256", AttnConfig("c9", 1, 2, 2, 128, 0, 512, 256)),
+    # trace replay: S noisy copies (reading c19)
+    ("copies2_gqa2_aligned", AttnConfig("t1", 1, 4, 2, 128, 64, 320, 4, n_copies=2)),
+    ("copies3_resp_only_ragged", AttnConfig("t2", 1, 2, 1, 128, 40, 200, 8, repeat_prompt=0, n_copies=3)),
+    ("copies4_d64_B1", AttnConfig("t3", 1, 2, 2, 64, 0, 136, 1, n_copies=4)),
+    ("copies2_B128", AttnConfig("t4", 1, 2, 1, 128, 128, 256, 128, n_copies=2)),
 ]
 
 
 def _oprob(cfg):
     return OProblem(cfg.batch, cfg.prompt_len, cfg.response_len, cfg.block_size, cfg.n_q_heads,
-                    cfg.n_kv_heads, cfg.head_dim, cfg.repeat_prompt)
+                    cfg.n_kv_heads, cfg.head_dim, cfg.repeat_prompt, n_copies=cfg.n_copies)
 
 
 def run_bwd(cfg, stress=False, structured_do=False):

@@ -21,12 +21,17 @@ CASES = [
     ("B32_d64_gqa2", AttnConfig("c7", 2, 4, 2, 64, 96, 416, 32)),
     ("tiny_L_lt_tile", AttnConfig("c8", 1, 2, 1, 128, 8, 24, 8)),
     ("big_block_B256", AttnConfig("c9", 1, 2, 2, 128, 0, 512, 256)),
+    # trace replay: S noisy copies (reading c19)
+    ("copies2_gqa2_aligned", AttnConfig("t1", 1, 4, 2, 128, 64, 320, 4, n_copies=2)),
+    ("copies3_resp_only_ragged", AttnConfig("t2", 1, 2, 1, 128, 40, 200, 8, repeat_prompt=0, n_copies=3)),
+    ("copies4_d64_B1", AttnConfig("t3", 1, 2, 2, 64, 0, 136, 1, n_copies=4)),
+    ("copies2_B128", AttnConfig("t4", 1, 2, 1, 128, 128, 256, 128, n_copies=2)),
 ]
 
 
 def _oprob(cfg):
     return OProblem(cfg.batch, cfg.prompt_len, cfg.response_len, cfg.block_size, cfg.n_q_heads,
-                    cfg.n_kv_heads, cfg.head_dim, cfg.repeat_prompt)
+                    cfg.n_kv_heads, cfg.head_dim, cfg.repeat_prompt, n_copies=cfg.n_copies)
 
 
 def _check_full(cfg, stress=False, seed=None):
@@ -75,3 +80,20 @@ def test_fwd_deterministic_and_x0_independent_of_xt(cuda_ok):
         x[:, L:] += 1.0
     o3, l3 = bd.attn_fwd(prob, q2, k2, v2)
     assert torch.equal(o1[:, :L], o3[:, :L]) and torch.equal(l1[:, :, :L], l3[:, :, :L])
+
+
+@pytest.mark.gpu
+def test_fwd_copies_equal_single_copy_runs(cuda_ok):
+    """Trace replay (reading c19): the rows of copy s from one expanded
+    launch are bit-identical to a single-copy launch over [x0 | copy s] (same
+    tile list in the same order)."""
+    cfg = AttnConfig("r", 2, 4, 2, 128, 64, 320, 4, n_copies=3)
+    prob = bd.Problem.from_cfg(cfg)
+    q, k, v, _ = attn_inputs(cfg, device="cuda", with_do=False)
+    o, lse = bd.attn_fwd(prob, q, k, v)
+    one = prob.with_(n_copies=1)
+    L, Lx = cfg.L, cfg.L - cfg.xb
+    for s in range(3):
+        idx = torch.cat([torch.arange(L), L + s * Lx + torch.arange(Lx)]).cuda()
+        o1, l1 = bd.attn_fwd(one, q[:, idx].contiguous(), k[:, idx].contiguous(), v[:, idx].contiguous())
+        assert torch.equal(o[:, idx], o1) and torch.equal(lse[:, :, idx], l1)

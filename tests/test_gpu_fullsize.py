@@ -26,7 +26,7 @@ from workloads import CONFIGS, attn_inputs, logits_inputs, VOCAB_QWEN3
 
 def _oprob(cfg):
     return OProblem(cfg.batch, cfg.prompt_len, cfg.response_len, cfg.block_size, cfg.n_q_heads,
-                    cfg.n_kv_heads, cfg.head_dim, cfg.repeat_prompt)
+                    cfg.n_kv_heads, cfg.head_dim, cfg.repeat_prompt, n_copies=cfg.n_copies)
 
 
 def _rows(cfg, n, seed):
@@ -41,7 +41,7 @@ def _slice(x, b, h):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["sdar_1_7b", "sdar_8b", "sweep_b8", "sweep_b32"])
+@pytest.mark.parametrize("name", ["sdar_1_7b", "sdar_8b", "sweep_b8", "sweep_b32", "trace_s4"])
 def test_fullsize_sampled_parity(cuda_ok, name):
     cfg = CONFIGS[name]
     prob = bd.Problem.from_cfg(cfg)
@@ -50,7 +50,8 @@ def test_fullsize_sampled_parity(cuda_ok, name):
     dq, dk, dv = bd.attn_bwd(prob, q, k, v, o, lse, do)
     torch.cuda.synchronize()
     G = cfg.n_q_heads // cfg.n_kv_heads
-    one = OProblem(1, cfg.prompt_len, cfg.response_len, cfg.block_size, 1, 1, cfg.head_dim, cfg.repeat_prompt)
+    one = OProblem(1, cfg.prompt_len, cfg.response_len, cfg.block_size, 1, 1, cfg.head_dim, cfg.repeat_prompt,
+                   n_copies=cfg.n_copies)
     rng = np.random.default_rng(7)
     # -- rows: (b, h) = (0, 0), (b-1, Hq-1), one random
     pairs = [(0, 0), (cfg.batch - 1, cfg.n_q_heads - 1), (int(rng.integers(cfg.batch)), int(rng.integers(cfg.n_q_heads)))]
@@ -77,7 +78,8 @@ def test_fullsize_sampled_parity(cuda_ok, name):
     # -- keys of one (sequence, kv head): last x0 block, a middle x0 key, xt keys
     b, g_ = cfg.batch - 1, cfg.n_kv_heads - 1
     L, N, B = cfg.L, cfg.ntot, cfg.block_size
-    keys = np.array([L - 1, L - B, L // 2 + 3, L + 5, N - 1, L + L // 2])
+    mid = L // 2 + 3 if cfg.n_copies == 1 else L - 3 * B - 1  # keep the oracle's row count small
+    keys = np.array([L - 1, L - B, mid, L + 5, N - 1, L + L // 2])
     vis = mask.mask_rows(one, np.arange(N))[:, keys]  # [N, n_keys]
     ks, vs = _slice(k, b, g_), _slice(v, b, g_)
     ref_dk = np.zeros((len(keys), cfg.head_dim))

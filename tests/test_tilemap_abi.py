@@ -75,6 +75,20 @@ def test_tilemap_bit_exact_vs_oracle(P, R, B, rp):
     assert got == ref
 
 
+@pytest.mark.parametrize("S", [2, 3])
+@pytest.mark.parametrize("P,R,B,rp", [c for i, c in enumerate(_cases()) if i % 2 == 0 or c[3] == 0])
+def test_tilemap_copies_bit_exact_vs_oracle(P, R, B, rp, S):
+    """Trace replay (S noisy copies, reading c19): same bit-exact bar."""
+    p = bd.Problem(1, P, R, B, 1, 1, 64, repeat_prompt=rp, n_copies=S)
+    assert bd.packed_len(p) == OProblem(1, P, R, B, 1, 1, 64, repeat_prompt=rp, n_copies=S).ntot == p.ntot
+    got = bd.tilemap_dump(p)
+    ref = tilemap.classify(OProblem(1, P, R, B, 1, 1, 64, repeat_prompt=rp, n_copies=S))
+    assert got == ref
+    c = ctypes.c_int64(-1)
+    if p.ntot <= 4096:
+        assert _lib.lib().bd_tilemap_selfcheck(ctypes.byref(p.c()), ctypes.byref(c)) == 0 and c.value == 0
+
+
 @pytest.mark.parametrize("name", ["sdar_1_7b", "sdar_8b", "sweep_b4", "sweep_b32"])
 def test_tilemap_configs_closed_form(name):
     """Aligned configs: T^2 + 2T non-empty of 4T^2, 3T PARTIAL."""

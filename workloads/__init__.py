@@ -36,6 +36,7 @@ class AttnConfig:
     block_size: int
     repeat_prompt: int = 1
     seed: int = 0
+    n_copies: int = 1  # S noisy copies: trace replay (reading c19)
 
     @property
     def L(self):
@@ -47,7 +48,7 @@ class AttnConfig:
 
     @property
     def ntot(self):
-        return 2 * self.L - self.xb
+        return self.L + self.n_copies * (self.L - self.xb)
 
     def with_(self, **kw):
         return replace(self, **kw)
@@ -63,6 +64,9 @@ CONFIGS = {
     "sweep_b32": AttnConfig("sweep_b32", 16, 32, 8, 128, 1024, 4096, 32, seed=3),
     # 8xB200 RL step: 128 prompts x group 8 = 1024 sequences, micro-batch 16
     "rl8_micro": AttnConfig("rl8_micro", 16, 32, 8, 128, 1024, 8192, 4, seed=4),
+    # trace replay: SDAR-8B shape, B = 4 decoded one token
+    # per step -> S = 4 noisy copies [x0 | xt(1) | .. | xt(4)], Ntot = 5 L
+    "trace_s4": AttnConfig("trace_s4", 16, 32, 8, 128, 1024, 8192, 4, seed=5, n_copies=4),
 }
 
 # logprob rows per config: N = b * R response rows
@@ -96,7 +100,9 @@ def attn_inputs(cfg: AttnConfig, device="cpu", seed=None, stress=False, dtype=to
             # zero on x0 rows and on noisy-prompt rows (loss only on the
             # repeated response)
             keep = torch.zeros(N, device=device, dtype=torch.float32)
-            keep[cfg.L + (cfg.prompt_len - cfg.xb):] = 1.0
+            Lx = cfg.L - cfg.xb
+            for c in range(cfg.n_copies):
+                keep[cfg.L + c * Lx + (cfg.prompt_len - cfg.xb):cfg.L + (c + 1) * Lx] = 1.0
             do = do * keep[None, :, None, None]
         do = do.to(dtype)
     return q, k, v, do
@@ -130,10 +136,11 @@ def rl_batch(n_groups, group_size, resp_lens, seed=0):
 
 def useful_pairs(cfg: AttnConfig) -> int:
     """Closed-form count of visible pairs per (sequence, head) in DiRL mode,
-    L (L + B) (derived); for response-only mode counted by the
-    caller from the oracle."""
+    L (L + B) (derived), (1 + S) L (L + B) / 2 with S noisy
+    copies (reading c19); for response-only mode counted by the caller from
+    the oracle."""
     assert cfg.repeat_prompt == 1
-    return cfg.L * (cfg.L + cfg.block_size)
+    return (1 + cfg.n_copies) * cfg.L * (cfg.L + cfg.block_size) // 2
 
 
 def useful_flops(cfg: AttnConfig, pairs=None):
