@@ -41,7 +41,7 @@ namespace {
 constexpr float kLog2e = 1.4426950408889634f;
 
 // ------------------------------------------------------------ preprocess
-// D_i = rowsum(dO_i o O_i) and log2-domain LSE, written tile-major.  One
+// -D_i = -rowsum(dO_i o O_i) and -log2-domain LSE, written tile-major.  One
 // 16-byte load per thread per tensor; D/8 threads per row; grid
 // (ceil(N / rows_per_block), b * Hq).
 template <int D>
@@ -73,8 +73,9 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
     const int t = tile_of_row(g, n);
     const int r = n - tile_start(g, t);
     const size_t slot = ((size_t)bh * g.NT + t) * kTileRows + r;
-    dsum_t[slot] = acc;
-    lse2_t[slot] = lse[(size_t)bh * N + n] * kLog2e;
+    // stored negated: the compute loops add them with packed FFMA2 / FADD2
+    dsum_t[slot] = -acc;
+    lse2_t[slot] = -lse[(size_t)bh * N + n] * kLog2e;
   }
 }
 
@@ -134,7 +135,12 @@ __device__ __forceinline__ void store_row_bf16_n(__nv_bfloat16* dst, const uint3
 template <bool MASKED, int NC>
 __device__ __forceinline__ void p_tile(const uint32_t* sr, const float* sv, float sl2, int ja, int jb, float* pv) {
 #pragma unroll
-  for (int j = 0; j < NC; ++j) pv[j] = ex2_mix(j, fmaf(__uint_as_float(sr[j]), sl2, -sv[j]));
+  for (int j = 0; j < NC; j += 2) {  // sv = -lse2 (negated by bwd_pre)
+    const float2 x = ffma2(make_float2(__uint_as_float(sr[j]), __uint_as_float(sr[j + 1])), make_float2(sl2, sl2),
+                           make_float2(sv[j], sv[j + 1]));
+    pv[j] = ex2_mix(j, x.x);
+    pv[j + 1] = ex2_mix(j + 1, x.y);
+  }
   if (MASKED) {
 #pragma unroll
     for (int j = 0; j < NC; ++j) pv[j] = (j >= ja && j < jb) ? pv[j] : 0.f;
@@ -142,9 +148,14 @@ __device__ __forceinline__ void p_tile(const uint32_t* sr, const float* sv, floa
 }
 // Same with a per-row lse2 (dQ kernel), 32 columns.
 template <bool MASKED>
-__device__ __forceinline__ void p_row(const uint32_t* sr, float lse2, float sl2, int ja, int jb, float* pv) {
+__device__ __forceinline__ void p_row(const uint32_t* sr, float nlse2, float sl2, int ja, int jb, float* pv) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j) pv[j] = ex2_mix(j, fmaf(__uint_as_float(sr[j]), sl2, -lse2));
+  for (int j = 0; j < 32; j += 2) {
+    const float2 x = ffma2(make_float2(__uint_as_float(sr[j]), __uint_as_float(sr[j + 1])), make_float2(sl2, sl2),
+                           make_float2(nlse2, nlse2));
+    pv[j] = ex2_mix(j, x.x);
+    pv[j + 1] = ex2_mix(j + 1, x.y);
+  }
   if (MASKED) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) pv[j] = (j >= ja && j < jb) ? pv[j] : 0.f;
@@ -425,8 +436,10 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
 #pragma unroll
         for (int j = 0; j < NC / 2; ++j) {
           const float p0 = pv[2 * j], p1 = pv[2 * j + 1];
-          dsk[j] = pack_bf16x2(p0 * (__uint_as_float(dr[2 * j]) - sv[128 + 2 * j]),
-                               p1 * (__uint_as_float(dr[2 * j + 1]) - sv[128 + 2 * j + 1]));
+          const float2 ds = fmul2(make_float2(p0, p1),
+                                  fadd2(make_float2(__uint_as_float(dr[2 * j]), __uint_as_float(dr[2 * j + 1])),
+                                        make_float2(sv[128 + 2 * j], sv[128 + 2 * j + 1])));  // sv = -D
+          dsk[j] = pack_bf16x2(ds.x, ds.y);
           pk[j] = pack_bf16x2(p0, p1);
         }
         tmem_st16(tP, pk);
@@ -693,8 +706,8 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
     row_interval(g, qseg, row, 0, lo0, hi0);
     row_interval(g, qseg, row, qseg ? qseg : 1, lo1, hi1);  // the row's own noisy copy
     const size_t vslot = (((size_t)b * a.n_q_heads + h) * g.NT + qt) * kTileRows + r;
-    const float lse2 = a.lse2_t[vslot];
-    const float dsum = a.dsum_t[vslot];
+    const float nlse2 = a.lse2_t[vslot];  // -lse2 and -D (negated by bwd_pre)
+    const float ndsum = a.dsum_t[vslot];
     for (int j = 0; j < n_kt; ++j) {
       const int ent = ents[j];
       const int kt = entry_tile(ent);
@@ -715,9 +728,9 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         tmem_ld32(sbase + cb, sr);
         tmem_ld_wait();
         if (need_mask)
-          p_row<true>(sr, lse2, sl2, lo - cb, hi - cb, pv);
+          p_row<true>(sr, nlse2, sl2, lo - cb, hi - cb, pv);
         else
-          p_row<false>(sr, lse2, sl2, 0, 32, pv);
+          p_row<false>(sr, nlse2, sl2, 0, 32, pv);
       }
       // phase 2: dS = P (dP - D) -> bf16 over the S columns already read
       mbar_wait(dp_full, j & 1);
@@ -734,8 +747,12 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         TRACE(4096 + 8 * (j & 127) + 2, blockIdx.x == 0 && threadIdx.x == 0);
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj)
-          pk[jj] = pack_bf16x2(pv[2 * jj] * (__uint_as_float(dr[2 * jj]) - dsum),
-                               pv[2 * jj + 1] * (__uint_as_float(dr[2 * jj + 1]) - dsum));
+        {
+          const float2 ds = fmul2(make_float2(pv[2 * jj], pv[2 * jj + 1]),
+                                  fadd2(make_float2(__uint_as_float(dr[2 * jj]), __uint_as_float(dr[2 * jj + 1])),
+                                        make_float2(ndsum, ndsum)));
+          pk[jj] = pack_bf16x2(ds.x, ds.y);
+        }
       }
       tmem_st16(sbase + cb, pk);
       tmem_st_wait();

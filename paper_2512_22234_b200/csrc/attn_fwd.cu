@@ -72,6 +72,14 @@ struct FwdArgs {
 // thread's row): optional interval mask [lo, hi), running max m (log2 units,
 // lazily raised by > 8), running sum l, P = 2^(s sl2 - m) written over tS as
 // bf16.  Returns the new max, whether O must be rescaled, and by how much.
+// Share of the forward's exps moved from the MUFU to the packed FMA-pipe
+// polynomial: element pair c uses it iff c % BD_FWD_POLY_MOD == MOD - 1
+// (0 = MUFU only).  At d = 128 the MUFU (16 ex2/clk/SM) needs as many clocks
+// per tile as the tensor core, so it co-bounds the forward.
+#ifndef BD_FWD_POLY_MOD
+#define BD_FWD_POLY_MOD 4
+#endif
+
 template <bool MASKED>
 __device__ __forceinline__ void softmax_tile(uint32_t tS, int lo, int hi, float sl2, float m, float& l,
                                              float& m_new, bool& resc, float& alpha) {
@@ -84,9 +92,17 @@ __device__ __forceinline__ void softmax_tile(uint32_t tS, int lo, int hi, float 
 #pragma unroll
     for (int c = 0; c < 128; ++c) s[c] = (c >= lo && c < hi) ? s[c] : -INFINITY;
   }
-  float mx = s[0];
+  // row max: 8 independent chains (a single FMNMX3 chain is ~64 dependent
+  // instructions with one softmax warp per scheduler to hide them)
+  float mx8[8];
 #pragma unroll
-  for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
+  for (int i = 0; i < 8; ++i) mx8[i] = s[i];
+#pragma unroll
+  for (int c = 8; c < 128; c += 8)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(mx8[i], s[c + i]);
+  const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
   const float tmax = mx * sl2;
   m_new = m;
   resc = false;
@@ -96,15 +112,24 @@ __device__ __forceinline__ void softmax_tile(uint32_t tS, int lo, int hi, float 
   }
   const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
   alpha = resc ? ex2_approx(m - m_use) : 1.f;
-  float sum = 0.f;
+  const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_use, -m_use);
+  float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
   uint32_t pk[64];
 #pragma unroll
   for (int c = 0; c < 64; ++c) {
-    const float p0 = ex2_mix(2 * c, fmaf(s[2 * c], sl2, -m_use));
-    const float p1 = ex2_mix(2 * c + 1, fmaf(s[2 * c + 1], sl2, -m_use));
-    sum += p0 + p1;
-    pk[c] = pack_bf16x2(p0, p1);
+    const float2 x = ffma2(make_float2(s[2 * c], s[2 * c + 1]), sl2v, nm);
+    float2 p;
+    if (BD_FWD_POLY_MOD > 0 && (c % BD_FWD_POLY_MOD) == BD_FWD_POLY_MOD - 1) {
+      p = ex2_poly2(x);
+    } else {
+      p.x = ex2_approx(x.x);
+      p.y = ex2_approx(x.y);
+    }
+    acc[c & 3] = fadd2(acc[c & 3], p);
+    pk[c] = pack_bf16x2(p.x, p.y);
   }
+  const float2 a01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+  const float sum = a01.x + a01.y;
   l = l * alpha + sum;
 #pragma unroll
   for (int c = 0; c < 2; ++c) tmem_st32(tS + 32 * c, pk + 32 * c);

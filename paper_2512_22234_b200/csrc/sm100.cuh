@@ -258,6 +258,43 @@ __device__ __forceinline__ float ex2_mix(int c, float x) {
   return ex2_approx(x);
 }
 
+// ---- packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 / FMUL2 -- one issue
+// slot for two lanes' worth of fp32 work; the softmax loops are issue-bound
+// once the MUFU is shared with the polynomial)
+__device__ __forceinline__ uint64_t f2_bits(float2 a) { return *reinterpret_cast<uint64_t*>(&a); }
+__device__ __forceinline__ float2 bits_f2(uint64_t r) { return *reinterpret_cast<float2*>(&r); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+  return bits_f2(d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(d);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(d);
+}
+
+// 2^x for a pair on the FMA pipe, packed (same fit as ex2_poly): ~5 issue
+// slots per element against the MUFU's 8-clock-per-warp ex2.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = fadd2(x, magic);
+  const float2 tm = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 r = ffma2(tm, make_float2(-1.f, -1.f), x);  // x - rint(x)
+  float2 p = ffma2(make_float2(0.05500893f, 0.05500893f), r, make_float2(0.24221098f, 0.24221098f));
+  p = ffma2(p, r, make_float2(0.69328293f, 0.69328293f));
+  p = ffma2(p, r, make_float2(1.0f, 1.0f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 // Byte offset of 16-byte chunk `chunk` (0..7) of row `row` inside a
 // 128B-swizzled tile whose rows are 128 B.
 __device__ __forceinline__ uint32_t sw128_offset(uint32_t row, uint32_t chunk) {
