@@ -78,6 +78,18 @@ typedef struct bd_problem {
                           * block's state before decoding step s; copy s of
                           * block k sees x0 blocks < k and itself only
                           * (reading c19)                      */
+  /* Varlen batch (RL responses vary in length, P:331,
+   * P:382): optional HOST arrays of `batch` per-sequence prompt / response
+   * lengths (both NULL = every sequence has prompt_len / response_len).
+   * Sequence i then has L_i = P_i + R_i (L_i % block_size == 0, 0 <= P_i <=
+   * prompt_len, 0 <= R_i <= response_len) and packed length
+   * N_i = L_i + S (L_i - xb_i) <= Ntot; tensors keep the padded [b, Ntot, H, d]
+   * layout and rows n >= N_i of sequence i are neither read for any output
+   * nor written (q/k/v/o/lse/dO there may hold anything; O/LSE/dQ/dK/dV there
+   * are left untouched).  The arrays are read during the call only (copied
+   * into a kernel parameter, no host->device transfer); batch <= 1024.     */
+  const int32_t* seq_prompt_len;
+  const int32_t* seq_response_len;
 } bd_problem;
 
 /* Packed length Ntot of one sequence, or -1 if the problem is invalid. */

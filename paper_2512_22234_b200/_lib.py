@@ -25,6 +25,8 @@ class BdProblem(ctypes.Structure):
         ("repeat_prompt", ctypes.c_int32),
         ("softmax_scale", ctypes.c_float),
         ("n_copies", ctypes.c_int32),
+        ("seq_prompt_len", ctypes.POINTER(ctypes.c_int32)),
+        ("seq_response_len", ctypes.POINTER(ctypes.c_int32)),
     ]
 
 

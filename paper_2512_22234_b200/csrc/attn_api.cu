@@ -9,21 +9,29 @@ namespace {
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
-  size_t map_off, dsum_off, dq_off, total;
+  size_t map_off, dsum_off, total;
+  int map_stride;  // words between per-sequence maps (varlen), 0 = one map
 };
 
 WsLayout ws_layout(const bd_problem& p, int backward) {
   const Geom g = geom_of(p);
   WsLayout w{};
   w.map_off = 0;
-  size_t off = align256((size_t)map_words(g) * sizeof(int));
+  const size_t one = (size_t)map_words(g);
+  w.map_stride = is_varlen(p) ? (int)((one + 63) & ~size_t(63)) : 0;
+  size_t off = align256((is_varlen(p) ? (size_t)w.map_stride * p.batch : one) * sizeof(int));
   if (backward) {
-    w.dsum_off = off;  // tile-major log2-LSE and D vectors
+    w.dsum_off = off;  // tile-major log2-LSE and D vectors (dQ accumulates in TMEM)
     off = align256(off + bwd_vec_floats(p, g) * sizeof(float));
-    w.dq_off = off;  // dQ is accumulated in TMEM: no fp32 accumulator needed
   }
   w.total = off;
   return w;
+}
+
+int build_maps(const bd_problem& p, const Geom& g, const WsLayout& wl, int* map, cudaStream_t stream) {
+  if (!is_varlen(p)) return build_map_device(g, map, stream);
+  const SeqLens lens = seq_lens_of(p);
+  return build_map_device_varlen(g, lens, map, wl.map_stride, stream);
 }
 
 int check_ptrs(std::initializer_list<const void*> ps) {
@@ -65,8 +73,8 @@ extern "C" int bd_attn_fwd(const bd_problem* prob, const void* q, const void* k,
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   const Geom g = geom_of(*prob);
   int* map = reinterpret_cast<int*>(static_cast<char*>(ws) + wl.map_off);
-  if ((rc = build_map_device(g, map, stream))) return rc;
-  return run_attn_fwd(*prob, g, q, k, v, o, lse, map, stream);
+  if ((rc = build_maps(*prob, g, wl, map, stream))) return rc;
+  return run_attn_fwd(*prob, g, q, k, v, o, lse, map, wl.map_stride, stream);
 }
 
 extern "C" int bd_attn_bwd(const bd_problem* prob, const void* q, const void* k, const void* v, const void* o,
@@ -83,7 +91,7 @@ extern "C" int bd_attn_bwd(const bd_problem* prob, const void* q, const void* k,
   const Geom g = geom_of(*prob);
   char* w = static_cast<char*>(ws);
   int* map = reinterpret_cast<int*>(w + wl.map_off);
-  if ((rc = build_map_device(g, map, stream))) return rc;
-  return run_attn_bwd(*prob, g, q, k, v, o, lse, dout, dq, dk, dv, map, reinterpret_cast<float*>(w + wl.dsum_off),
-                      reinterpret_cast<float*>(w + wl.dq_off), stream);
+  if ((rc = build_maps(*prob, g, wl, map, stream))) return rc;
+  return run_attn_bwd(*prob, g, q, k, v, o, lse, dout, dq, dk, dv, map, wl.map_stride,
+                      reinterpret_cast<float*>(w + wl.dsum_off), stream);
 }

@@ -44,19 +44,23 @@ constexpr float kLog2e = 1.4426950408889634f;
 // -D_i = -rowsum(dO_i o O_i) and -log2-domain LSE, written tile-major.  One
 // 16-byte load per thread per tensor; D/8 threads per row; grid
 // (ceil(N / rows_per_block), b * Hq).
-template <int D>
+template <int D, bool VARLEN>
 __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __restrict__ o,
                                                       const __nv_bfloat16* __restrict__ dout,
                                                       const float* __restrict__ lse, float* __restrict__ lse2_t,
-                                                      float* __restrict__ dsum_t, int N, int Hq, Geom g) {
+                                                      float* __restrict__ dsum_t, int N, int Hq, Geom gm,
+                                                      const int* __restrict__ map, int map_stride) {
   constexpr int kTpr = D / 8;             // threads per row
   constexpr int kRows = 256 / kTpr;       // rows per block
   const int bh = blockIdx.y;
   const int b = bh / Hq, h = bh - b * Hq;
   const int n = blockIdx.x * kRows + threadIdx.x / kTpr;
   const int sub = threadIdx.x % kTpr;
+  // varlen: rows past this sequence's packed length are padding
+  const Geom g = VARLEN ? map_geom(map + (size_t)b * map_stride) : gm;
+  const bool valid = n < (VARLEN ? g.N : N);
   float acc = 0.f;
-  if (n < N) {
+  if (valid) {
     const size_t base = (((size_t)b * N + n) * Hq + h) * D + sub * 8;
     const uint4 a = *reinterpret_cast<const uint4*>(o + base);
     const uint4 c = *reinterpret_cast<const uint4*>(dout + base);
@@ -69,10 +73,10 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
   }
 #pragma unroll
   for (int off = kTpr / 2; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (n < N && sub == 0) {
+  if (valid && sub == 0) {
     const int t = tile_of_row(g, n);
     const int r = n - tile_start(g, t);
-    const size_t slot = ((size_t)bh * g.NT + t) * kTileRows + r;
+    const size_t slot = ((size_t)bh * gm.NT + t) * kTileRows + r;  // stride: the batch's max tile count
     // stored negated: the compute loops add them with packed FFMA2 / FADD2
     dsum_t[slot] = -acc;
     lse2_t[slot] = -lse[(size_t)bh * N + n] * kLog2e;
@@ -95,6 +99,7 @@ __device__ long long g_trace[8192];
 
 struct BwdArgs {
   const int* map;
+  int map_stride;  // varlen: words between per-sequence maps
   const float* lse2_t;
   const float* dsum_t;
   __nv_bfloat16* dq;
@@ -132,14 +137,30 @@ __device__ __forceinline__ void store_row_bf16_n(__nv_bfloat16* dst, const uint3
 // P = 2^(s sl2 - lse2) for NC columns, zeroed outside [ja, jb) when MASKED
 // (dK/dV kernel: per-column lse2 from smem).  Masked and unmasked tiles take
 // separate code paths so FULL tiles pay no per-element mask work.
+// Share of the exps on the packed FMA-pipe polynomial (pair j/2 uses it iff
+// (j/2) % MOD == MOD - 1; 0 = MUFU only), per kernel.
+#ifndef BD_DKDV_POLY_MOD
+#define BD_DKDV_POLY_MOD 0
+#endif
+#ifndef BD_DQ_POLY_MOD
+#define BD_DQ_POLY_MOD 0
+#endif
+
+template <int MOD>
+__device__ __forceinline__ float2 ex2_pair(int pair, float2 x) {
+  if (MOD > 0 && (pair % MOD) == MOD - 1) return ex2_poly2(x);
+  return make_float2(ex2_approx(x.x), ex2_approx(x.y));
+}
+
 template <bool MASKED, int NC>
 __device__ __forceinline__ void p_tile(const uint32_t* sr, const float* sv, float sl2, int ja, int jb, float* pv) {
 #pragma unroll
   for (int j = 0; j < NC; j += 2) {  // sv = -lse2 (negated by bwd_pre)
     const float2 x = ffma2(make_float2(__uint_as_float(sr[j]), __uint_as_float(sr[j + 1])), make_float2(sl2, sl2),
                            make_float2(sv[j], sv[j + 1]));
-    pv[j] = ex2_mix(j, x.x);
-    pv[j + 1] = ex2_mix(j + 1, x.y);
+    const float2 p = ex2_pair<BD_DKDV_POLY_MOD>(j / 2, x);
+    pv[j] = p.x;
+    pv[j + 1] = p.y;
   }
   if (MASKED) {
 #pragma unroll
@@ -153,8 +174,9 @@ __device__ __forceinline__ void p_row(const uint32_t* sr, float nlse2, float sl2
   for (int j = 0; j < 32; j += 2) {
     const float2 x = ffma2(make_float2(__uint_as_float(sr[j]), __uint_as_float(sr[j + 1])), make_float2(sl2, sl2),
                            make_float2(nlse2, nlse2));
-    pv[j] = ex2_mix(j, x.x);
-    pv[j + 1] = ex2_mix(j + 1, x.y);
+    const float2 p = ex2_pair<BD_DQ_POLY_MOD>(j / 2, x);
+    pv[j] = p.x;
+    pv[j + 1] = p.y;
   }
   if (MASKED) {
 #pragma unroll
@@ -200,7 +222,7 @@ struct DkdvCfg {
   static_assert(kSmemBytes <= 232448, "dkdv smem budget");
 };
 
-template <int D>
+template <int D, bool VARLEN>
 __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
     attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                          const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -228,16 +250,20 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
-  const Geom& g = a.g;
+  const Geom& gm = a.g;  // the batch's (maximum) geometry: grid, vector strides
   if ((smem_u32(smem) & 1023u) != 0) __trap();
 
   // Grid order: (sequence, kv head) outermost, LPT rank of the k-tile inner --
   // concurrently resident CTAs stream the same Q / dO tiles (L2 reuse).
-  const int unit = blockIdx.x / g.NT;
-  const int rank = blockIdx.x - unit * g.NT;
+  const int unit = blockIdx.x / gm.NT;
+  const int rank = blockIdx.x - unit * gm.NT;
   const int b = unit / a.n_kv_heads;
   const int kvh = unit - b * a.n_kv_heads;
-  const MapView mv{const_cast<int*>(a.map), g.NT, map_capacity(g)};
+  const int* mapb = VARLEN ? a.map + (size_t)b * a.map_stride : a.map;
+  const Geom gsq = VARLEN ? map_geom(mapb) : gm;
+  const Geom& g = VARLEN ? gsq : gm;
+  if (VARLEN && rank >= g.NT) return;
+  const MapView mv{const_cast<int*>(mapb), g.NT, map_capacity(g)};
   const int kt = mv.bwd_order()[rank];
   const int e0 = mv.col_ptr()[kt];
   const int n_qt = mv.col_ptr()[kt + 1] - e0;
@@ -298,7 +324,7 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
         const int vs = i & 1;
         mbar_wait(&vec_empty[vs], ((i >> 1) & 1) ^ 1);
         mbar_expect_tx(&vec_full[vs], C::kVecBytes);
-        const size_t vec = (((size_t)b * a.n_q_heads + h) * g.NT + qt) * kTileRows;
+        const size_t vec = (((size_t)b * a.n_q_heads + h) * gm.NT + qt) * kTileRows;
         float* sv = reinterpret_cast<float*>(smem + C::kOffVec + vs * C::kVecBytes);
         bulk_load(sv, a.lse2_t + vec, 512, &vec_full[vs]);
         bulk_load(sv + 128, a.dsum_t + vec, 512, &vec_full[vs]);
@@ -534,7 +560,7 @@ __device__ __forceinline__ uint32_t dq_ring_phase(int idx) {
   return (uint32_t)(((idx & 1) ? j / C::kVSlots : j / C::kKSlots) & 1);
 }
 
-template <int D>
+template <int D, bool VARLEN>
 __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -557,19 +583,23 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
-  const Geom& g = a.g;
+  const Geom& gm = a.g;  // the batch's (maximum) geometry: grid, vector strides
   if ((smem_u32(smem) & 1023u) != 0) __trap();
 
   // Grid order: (sequence, kv head) outermost, then the q-tile's LPT rank,
   // then the q-heads of the group (they share every K/V tile: L2 reuse).
-  const int per_unit = g.NT * a.group;
+  const int per_unit = gm.NT * a.group;
   const int unit = blockIdx.x / per_unit;
   const int rem = blockIdx.x - unit * per_unit;
   const int rank = rem / a.group;
   const int b = unit / a.n_kv_heads;
   const int kvh = unit - b * a.n_kv_heads;
   const int h = kvh * a.group + (rem - rank * a.group);
-  const MapView mv{const_cast<int*>(a.map), g.NT, map_capacity(g)};
+  const int* mapb = VARLEN ? a.map + (size_t)b * a.map_stride : a.map;
+  const Geom gsq = VARLEN ? map_geom(mapb) : gm;
+  const Geom& g = VARLEN ? gsq : gm;
+  if (VARLEN && rank >= g.NT) return;
+  const MapView mv{const_cast<int*>(mapb), g.NT, map_capacity(g)};
   const int qt = mv.fwd_order()[rank];
   const int e0 = mv.row_ptr()[qt];
   const int n_kt = mv.row_ptr()[qt + 1] - e0;
@@ -705,7 +735,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
     int lo0, hi0, lo1, hi1;
     row_interval(g, qseg, row, 0, lo0, hi0);
     row_interval(g, qseg, row, qseg ? qseg : 1, lo1, hi1);  // the row's own noisy copy
-    const size_t vslot = (((size_t)b * a.n_q_heads + h) * g.NT + qt) * kTileRows + r;
+    const size_t vslot = (((size_t)b * a.n_q_heads + h) * gm.NT + qt) * kTileRows + r;
     const float nlse2 = a.lse2_t[vslot];  // -lse2 and -D (negated by bwd_pre)
     const float ndsum = a.dsum_t[vslot];
     for (int j = 0; j < n_kt; ++j) {
@@ -789,10 +819,10 @@ int set_smem(K kernel, int bytes, bool& done) {
   return BD_OK;
 }
 
-template <int D>
+template <int D, bool VARLEN>
 int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, const void* o,
-               const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, float* vec_ws,
-               cudaStream_t stream) {
+               const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, int map_stride,
+               float* vec_ws, cudaStream_t stream) {
   const int Hq = p.n_q_heads;
   const size_t nvec = (size_t)p.batch * Hq * g.NT * kTileRows;
   float* lse2_t = vec_ws;
@@ -802,20 +832,21 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   {
     constexpr int kRows = 256 / (D / 8);
     dim3 grid((g.N + kRows - 1) / kRows, p.batch * Hq);
-    bwd_pre_kernel<D><<<grid, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
-                                                 reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2_t, dsum_t,
-                                                 g.N, Hq, g);
+    bwd_pre_kernel<D, VARLEN><<<grid, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
+                                                         reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2_t,
+                                                         dsum_t, g.N, Hq, g, map, map_stride);
   }
   CUtensorMap tmQ, tmK, tmV, tmDO;
   if (!make_qkv_tmap(&tmQ, q, p.batch, g.N, Hq, D) || !make_qkv_tmap(&tmK, k, p.batch, g.N, p.n_kv_heads, D) ||
       !make_qkv_tmap(&tmV, v, p.batch, g.N, p.n_kv_heads, D) || !make_qkv_tmap(&tmDO, dout, p.batch, g.N, Hq, D))
     return set_error(BD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   static bool attr_kv = false, attr_q = false;
-  int rc = set_smem(attn_bwd_dkdv_kernel<D>, DkdvCfg<D>::kSmemBytes, attr_kv);
+  int rc = set_smem(attn_bwd_dkdv_kernel<D, VARLEN>, DkdvCfg<D>::kSmemBytes, attr_kv);
   if (rc) return rc;
-  if ((rc = set_smem(attn_bwd_dq_kernel<D>, DqCfg<D>::kSmemBytes, attr_q))) return rc;
+  if ((rc = set_smem(attn_bwd_dq_kernel<D, VARLEN>, DqCfg<D>::kSmemBytes, attr_q))) return rc;
   BwdArgs a;
   a.map = map;
+  a.map_stride = map_stride;
   a.lse2_t = lse2_t;
   a.dsum_t = dsum_t;
   a.dq = reinterpret_cast<__nv_bfloat16*>(dq);
@@ -833,13 +864,13 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   a.trace = trace_on ? 1 : 0;
   // 2. dK, dV
   const long long grid_kv = (long long)g.NT * p.batch * p.n_kv_heads;
-  attn_bwd_dkdv_kernel<D><<<(unsigned)grid_kv, DkdvCfg<D>::kThreads, DkdvCfg<D>::kSmemBytes, stream>>>(
+  attn_bwd_dkdv_kernel<D, VARLEN><<<(unsigned)grid_kv, DkdvCfg<D>::kThreads, DkdvCfg<D>::kSmemBytes, stream>>>(
       tmQ, tmK, tmV, tmDO, a);
   if ((rc = check_cuda(cudaGetLastError(), "attn_bwd_dkdv_kernel launch"))) return rc;
   // 3. dQ
   const long long grid_q = (long long)g.NT * p.batch * Hq;
   if (grid_q > 0x7FFFFFFF) return set_error(BD_ERR_UNSUPPORTED, "grid too large");
-  attn_bwd_dq_kernel<D><<<(unsigned)grid_q, DqCfg<D>::kThreads, DqCfg<D>::kSmemBytes, stream>>>(tmQ, tmK, tmV,
+  attn_bwd_dq_kernel<D, VARLEN><<<(unsigned)grid_q, DqCfg<D>::kThreads, DqCfg<D>::kSmemBytes, stream>>>(tmQ, tmK, tmV,
                                                                                                tmDO, a);
   note_launches(4);  // zero, pre, dkdv, dq
   return check_cuda(cudaGetLastError(), "attn_bwd_dq_kernel launch");
@@ -852,10 +883,15 @@ size_t bwd_vec_floats(const bd_problem& p, const Geom& g) {
 }
 
 int run_attn_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, const void* o,
-                 const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, float* vec_ws,
-                 float* /*unused*/, cudaStream_t stream) {
-  if (p.head_dim == 128) return launch_bwd<128>(p, g, q, k, v, o, lse, dout, dq, dk, dv, map, vec_ws, stream);
-  if (p.head_dim == 64) return launch_bwd<64>(p, g, q, k, v, o, lse, dout, dq, dk, dv, map, vec_ws, stream);
+                 const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, int map_stride,
+                 float* vec_ws, cudaStream_t stream) {
+  const bool vl = map_stride != 0;
+#define BD_BWD_CASE(D_)                                                                                  \
+  return vl ? launch_bwd<D_, true>(p, g, q, k, v, o, lse, dout, dq, dk, dv, map, map_stride, vec_ws, stream) \
+            : launch_bwd<D_, false>(p, g, q, k, v, o, lse, dout, dq, dk, dv, map, map_stride, vec_ws, stream)
+  if (p.head_dim == 128) BD_BWD_CASE(128);
+  if (p.head_dim == 64) BD_BWD_CASE(64);
+#undef BD_BWD_CASE
   return set_error(BD_ERR_UNSUPPORTED, "head_dim %d not in {64, 128}", p.head_dim);
 }
 

@@ -18,11 +18,13 @@ inline bool make_qkv_tmap(CUtensorMap* m, const void* base, int batch, int N, in
 }
 
 int build_map_device(const Geom& g, int* ws, cudaStream_t stream);
+int build_map_device_varlen(const Geom& gmax, const SeqLens& lens, int* ws, long long stride, cudaStream_t stream);
+// map_stride: words between consecutive sequences' maps (0 = one shared map)
 int run_attn_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, void* o,
-                 float* lse, const int* map, cudaStream_t stream);
+                 float* lse, const int* map, int map_stride, cudaStream_t stream);
 int run_attn_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, const void* o,
-                 const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, float* vec_ws,
-                 float* dq_acc, cudaStream_t stream);
+                 const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, int map_stride,
+                 float* vec_ws, cudaStream_t stream);
 size_t bwd_vec_floats(const bd_problem& p, const Geom& g);
 
 }  // namespace bd

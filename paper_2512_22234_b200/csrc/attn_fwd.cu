@@ -60,6 +60,7 @@ __device__ long long g_trace_fwd[8192];
 
 struct FwdArgs {
   const int* map;
+  int map_stride;  // varlen: words between per-sequence maps
   __nv_bfloat16* o;
   float* lse;
   int batch, n_q_heads, n_hg, group, N, n_kv;
@@ -135,7 +136,7 @@ __device__ __forceinline__ void softmax_tile(uint32_t tS, int lo, int hi, float 
   for (int c = 0; c < 2; ++c) tmem_st32(tS + 32 * c, pk + 32 * c);
 }
 
-template <int D, int NQ>
+template <int D, int NQ, bool VARLEN>
 __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const FwdArgs a) {
@@ -154,21 +155,26 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
-  const Geom& g = a.g;
+  const Geom& gm = a.g;  // the batch's (maximum) geometry: grid decomposition
 
   // ---- work unit: LPT rank of the q-tile, then (sequence, head pair)
   // Grid order: (sequence, kv head) outermost, then the q-tile's LPT rank,
   // then the head pairs of the group -- concurrently resident CTAs belong to
   // the same (sequence, kv head) and stream the same K/V tiles (L2 reuse).
   const int hp_per_kv = a.group / NQ;
-  const int per_unit = g.NT * hp_per_kv;
+  const int per_unit = gm.NT * hp_per_kv;
   const int unit = blockIdx.x / per_unit;
   const int rem = blockIdx.x - unit * per_unit;
   const int rank = rem / hp_per_kv;
   const int b = unit / a.n_kv;
   const int kvh = unit - b * a.n_kv;
   const int h0 = kvh * a.group + (rem - rank * hp_per_kv) * NQ;
-  const MapView mv{const_cast<int*>(a.map), g.NT, map_capacity(g)};
+  // varlen: this sequence's own map and geometry; ranks past its tile count exit
+  const int* mapb = VARLEN ? a.map + (size_t)b * a.map_stride : a.map;
+  const Geom gsq = VARLEN ? map_geom(mapb) : gm;
+  const Geom& g = VARLEN ? gsq : gm;
+  if (VARLEN && rank >= g.NT) return;
+  const MapView mv{const_cast<int*>(mapb), g.NT, map_capacity(g)};
   const int qt = mv.fwd_order()[rank];
   const int e0 = mv.row_ptr()[qt];
   const int n_kt = mv.row_ptr()[qt + 1] - e0;
@@ -365,9 +371,9 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
   if (warp == 0) tmem_dealloc<C::kTmemCols>(tbase);
 }
 
-template <int D, int NQ>
+template <int D, int NQ, bool VARLEN>
 int launch_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, void* o,
-               float* lse, const int* map, cudaStream_t stream) {
+               float* lse, const int* map, int map_stride, cudaStream_t stream) {
   using C = FwdCfg<D, NQ>;
   CUtensorMap tmQ, tmK, tmV;
   if (!make_qkv_tmap(&tmQ, q, p.batch, g.N, p.n_q_heads, D) || !make_qkv_tmap(&tmK, k, p.batch, g.N, p.n_kv_heads, D) ||
@@ -375,13 +381,14 @@ int launch_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
     return set_error(BD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, NQ, VARLEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(fwd)");
     attr = true;
   }
   FwdArgs a;
   a.map = map;
+  a.map_stride = map_stride;
   a.o = reinterpret_cast<__nv_bfloat16*>(o);
   a.lse = lse;
   a.batch = p.batch;
@@ -396,7 +403,7 @@ int launch_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   a.trace = trace_on ? 1 : 0;
   const long long grid = (long long)g.NT * p.batch * a.n_hg;
   if (grid > 0x7FFFFFFF) return set_error(BD_ERR_UNSUPPORTED, "grid too large");
-  attn_fwd_kernel<D, NQ><<<(unsigned)grid, C::kThreads, C::kSmemBytes, stream>>>(tmQ, tmK, tmV, a);
+  attn_fwd_kernel<D, NQ, VARLEN><<<(unsigned)grid, C::kThreads, C::kSmemBytes, stream>>>(tmQ, tmK, tmV, a);
   note_launches(1);
   return check_cuda(cudaGetLastError(), "attn_fwd_kernel launch");
 }
@@ -404,12 +411,21 @@ int launch_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
 }  // namespace
 
 int run_attn_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, void* o,
-                 float* lse, const int* map, cudaStream_t stream) {
+                 float* lse, const int* map, int map_stride, cudaStream_t stream) {
   const bool pair = (p.n_q_heads / p.n_kv_heads) % 2 == 0;
-  if (p.head_dim == 128) return pair ? launch_fwd<128, 2>(p, g, q, k, v, o, lse, map, stream)
-                                     : launch_fwd<128, 1>(p, g, q, k, v, o, lse, map, stream);
-  if (p.head_dim == 64) return pair ? launch_fwd<64, 2>(p, g, q, k, v, o, lse, map, stream)
-                                    : launch_fwd<64, 1>(p, g, q, k, v, o, lse, map, stream);
+  const bool vl = map_stride != 0;
+#define BD_FWD_CASE(D_, NQ_)                                                                         \
+  return vl ? launch_fwd<D_, NQ_, true>(p, g, q, k, v, o, lse, map, map_stride, stream)             \
+            : launch_fwd<D_, NQ_, false>(p, g, q, k, v, o, lse, map, map_stride, stream)
+  if (p.head_dim == 128) {
+    if (pair) BD_FWD_CASE(128, 2);
+    BD_FWD_CASE(128, 1);
+  }
+  if (p.head_dim == 64) {
+    if (pair) BD_FWD_CASE(64, 2);
+    BD_FWD_CASE(64, 1);
+  }
+#undef BD_FWD_CASE
   return set_error(BD_ERR_UNSUPPORTED, "head_dim %d not in {64, 128}", p.head_dim);
 }
 

@@ -29,12 +29,43 @@ inline int validate_problem(const bd_problem* p) {
   const int64_t NT = (L + kTileRows - 1) / kTileRows + S * ((Lx + kTileRows - 1) / kTileRows);
   if (NT > kMaxTiles) return set_error(BD_ERR_UNSUPPORTED, "sequence too long for the tile map (%lld tiles)",
                                        (long long)NT);
+  if ((p->seq_prompt_len == nullptr) != (p->seq_response_len == nullptr))
+    return set_error(BD_ERR_INVALID_ARG, "seq_prompt_len and seq_response_len must both be set or both null");
+  if (p->seq_prompt_len) {
+    if (p->batch > kMaxVarlenSeqs)
+      return set_error(BD_ERR_UNSUPPORTED, "varlen batch %d > %d sequences", p->batch, kMaxVarlenSeqs);
+    for (int i = 0; i < p->batch; ++i) {
+      const int Pi = p->seq_prompt_len[i], Ri = p->seq_response_len[i];
+      if (Pi < 0 || Ri < 0 || Pi > p->prompt_len || Ri > p->response_len)
+        return set_error(BD_ERR_INVALID_ARG, "sequence %d: lengths (%d, %d) outside [0, (%d, %d)]", i, Pi, Ri,
+                         p->prompt_len, p->response_len);
+      if (Pi + Ri <= 0) return set_error(BD_ERR_INVALID_ARG, "sequence %d is empty", i);
+      if ((Pi + Ri) % p->block_size)
+        return set_error(BD_ERR_LAYOUT, "sequence %d: L = %d not a multiple of block_size %d", i, Pi + Ri,
+                         p->block_size);
+    }
+  }
   return BD_OK;
 }
 
 inline Geom geom_of(const bd_problem& p) {
   const int L = p.prompt_len + p.response_len;
   return make_geom(L, p.repeat_prompt ? 0 : p.prompt_len, p.block_size, p.n_copies);
+}
+
+inline bool is_varlen(const bd_problem& p) { return p.seq_prompt_len != nullptr; }
+
+inline SeqLens seq_lens_of(const bd_problem& p) {
+  SeqLens s;
+  s.n = p.batch;
+  s.repeat_prompt = p.repeat_prompt;
+  s.B = p.block_size;
+  s.S = p.n_copies > 1 ? p.n_copies : 1;
+  for (int i = 0; i < p.batch; ++i) {
+    s.P[i] = p.seq_prompt_len[i];
+    s.R[i] = p.seq_response_len[i];
+  }
+  return s;
 }
 
 inline float scale_of(const bd_problem& p) {

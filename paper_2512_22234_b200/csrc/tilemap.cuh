@@ -197,7 +197,7 @@ __host__ __device__ inline int entry_kind(int e) { return (e >> 28) & 0xF; }
 
 // Workspace image of the map (int32 words):
 //   [0]            magic
-//   [1..7]         L, xb, B, NT, T0, n_entries, max_row_len
+//   [1..8]         L, xb, B, NT, T0, n_entries, max_row_len, S
 //   row_ptr[NT+1]  entries of q-tile t are row_ent[row_ptr[t] .. row_ptr[t+1])
 //   row_ent[cap]   k-tiles in increasing order
 //   col_ptr[NT+1]  column CSR (q-tiles visiting k-tile t), for the backward
@@ -205,7 +205,7 @@ __host__ __device__ inline int entry_kind(int e) { return (e >> 28) & 0xF; }
 //   fwd_order[NT]  q-tiles by decreasing row length (longest first, LPT)
 //   bwd_order[NT]  k-tiles by decreasing column length
 constexpr int kMapMagic = 0x42444D31;  // "BDM1"
-constexpr int kMapHeader = 8;
+constexpr int kMapHeader = 16;  // [8] = S (noisy copies); [9..15] reserved
 
 struct MapView {
   int* base;
@@ -227,6 +227,23 @@ __host__ __device__ inline int map_capacity(const Geom& g) {
 }
 __host__ __device__ inline long long map_words(const Geom& g) {
   return (long long)kMapHeader + 2LL * (g.NT + 1) + 2LL * map_capacity(g) + 2LL * g.NT;
+}
+
+// Geometry of the sequence whose map starts at `base` (varlen batches keep
+// one map per sequence; the kernels read their sequence's geometry from it).
+__host__ __device__ inline Geom map_geom(const int* base) { return make_geom(base[1], base[2], base[3], base[8]); }
+
+// Per-sequence lengths of a varlen batch, passed by
+// value to the map builder (kernel parameter: no host->device copy, no sync).
+constexpr int kMaxVarlenSeqs = 1024;
+struct SeqLens {
+  int n, repeat_prompt, B, S;
+  int P[kMaxVarlenSeqs];
+  int R[kMaxVarlenSeqs];
+};
+__host__ __device__ inline Geom seq_geom(const SeqLens& s, int i) {
+  const int L = s.P[i] + s.R[i];
+  return make_geom(L, s.repeat_prompt ? 0 : s.P[i], s.B, s.S);
 }
 
 }  // namespace bd

@@ -21,6 +21,7 @@ void build_map_host(const Geom& g, std::vector<int>& w) {
   w[3] = g.B;
   w[4] = g.NT;
   w[5] = g.T0;
+  w[8] = g.S;
   int n = 0, maxrow = 0;
   std::vector<int> rowlen(g.NT), collen(g.NT, 0);
   for (int t = 0; t < g.NT; ++t) {
@@ -114,7 +115,7 @@ __device__ int classify_pair_warp(const Geom& g, int qt, int kt, const int* s_lo
 
 // One warp per q-tile (strided).  Shared memory: rowlen[NT], collen[NT],
 // colfill[NT], scan scratch[1024], and per warp 4 x 128 ints of row intervals.
-__global__ void __launch_bounds__(kBuildThreads, 1) build_map_kernel(Geom g, int* __restrict__ ws) {
+__device__ void build_map_body(const Geom& g, int* __restrict__ ws) {
   extern __shared__ int sh[];
   const int NT = g.NT;
   int* rowlen = sh;                 // NT
@@ -199,7 +200,18 @@ __global__ void __launch_bounds__(kBuildThreads, 1) build_map_kernel(Geom g, int
     ws[5] = g.T0;
     ws[6] = mv.row_ptr()[NT];
     ws[7] = maxrow;
+    ws[8] = g.S;
   }
+}
+
+__global__ void __launch_bounds__(kBuildThreads, 1) build_map_kernel(Geom g, int* __restrict__ ws) {
+  build_map_body(g, ws);
+}
+
+// Varlen: CTA i builds sequence i's map at ws + i * stride.
+__global__ void __launch_bounds__(kBuildThreads, 1)
+    build_map_varlen_kernel(const __grid_constant__ SeqLens lens, int* __restrict__ ws, long long stride) {
+  build_map_body(seq_geom(lens, blockIdx.x), ws + blockIdx.x * stride);
 }
 
 }  // namespace
@@ -215,6 +227,19 @@ int build_map_device(const Geom& g, int* ws, cudaStream_t stream) {
   build_map_kernel<<<1, kBuildThreads, smem, stream>>>(g, ws);
   note_launches(1);
   return check_cuda(cudaGetLastError(), "build_map_kernel launch");
+}
+
+int build_map_device_varlen(const Geom& gmax, const SeqLens& lens, int* ws, long long stride, cudaStream_t stream) {
+  const size_t smem = (3 * (size_t)gmax.NT + kBuildThreads + (kBuildThreads / 32) * 512) * sizeof(int);
+  if (gmax.NT > kMaxTiles) return set_error(BD_ERR_UNSUPPORTED, "too many tiles (%d > %d)", gmax.NT, kMaxTiles);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(build_map_varlen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_done = true;
+  }
+  build_map_varlen_kernel<<<lens.n, kBuildThreads, smem, stream>>>(lens, ws, stride);
+  note_launches(1);
+  return check_cuda(cudaGetLastError(), "build_map_varlen_kernel launch");
 }
 
 }  // namespace bd

@@ -32,6 +32,10 @@ class Problem:
     repeat_prompt: int = 1
     softmax_scale: float = 0.0
     n_copies: int = 1  # S noisy copies (trace replay, reading c19)
+    # varlen batch: per-sequence prompt / response lengths (tuples of `batch`
+    # ints, both None = uniform); prompt_len / response_len are the maxima
+    seq_prompt_lens: tuple = None
+    seq_response_lens: tuple = None
 
     @property
     def L(self):
@@ -50,9 +54,27 @@ class Problem:
         return self.softmax_scale if self.softmax_scale > 0 else 1.0 / math.sqrt(self.head_dim)
 
     def c(self):
-        return BdProblem(self.batch, self.prompt_len, self.response_len, self.block_size, self.n_q_heads,
-                         self.n_kv_heads, self.head_dim, self.repeat_prompt, float(self.softmax_scale),
-                         self.n_copies)
+        st = BdProblem(self.batch, self.prompt_len, self.response_len, self.block_size, self.n_q_heads,
+                       self.n_kv_heads, self.head_dim, self.repeat_prompt, float(self.softmax_scale),
+                       self.n_copies)
+        if self.seq_prompt_lens is not None or self.seq_response_lens is not None:
+            arrs = []
+            for name, vals in (("seq_prompt_len", self.seq_prompt_lens), ("seq_response_len", self.seq_response_lens)):
+                if vals is None:
+                    continue
+                arr = (ctypes.c_int32 * len(vals))(*[int(x) for x in vals])
+                arrs.append(arr)
+                setattr(st, name, ctypes.cast(arr, ctypes.POINTER(ctypes.c_int32)))
+            st._keep = arrs  # the arrays must outlive the call
+        return st
+
+    def seq_packed_len(self, i):
+        """Packed length N_i of sequence i of a varlen batch."""
+        if self.seq_prompt_lens is None:
+            return self.ntot
+        P, R = self.seq_prompt_lens[i], self.seq_response_lens[i]
+        L = P + R
+        return L + max(self.n_copies, 1) * (L - (0 if self.repeat_prompt else P))
 
     def with_(self, **kw):
         return replace(self, **kw)

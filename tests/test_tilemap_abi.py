@@ -121,3 +121,20 @@ def test_row_and_key_intervals_agree(P, R, B, rp):
     n = ctypes.c_int64(-1)
     assert _lib.lib().bd_tilemap_selfcheck(ctypes.byref(p), ctypes.byref(n)) == 0
     assert n.value == 0
+
+
+def test_varlen_validation_and_workspace():
+    """Per-sequence lengths are checked on the host (S:214 layout errors)."""
+    L = _lib.lib()
+    ok = bd.Problem(3, 64, 320, 4, 4, 2, 128, seq_prompt_lens=(64, 32, 0), seq_response_lens=(320, 96, 200))
+    assert bd.packed_len(ok) == 2 * 384
+    ws_u = bd.workspace_bytes(bd.Problem(3, 64, 320, 4, 4, 2, 128), True)
+    assert bd.workspace_bytes(ok, True) > ws_u > 0  # one map per sequence
+    for P_, R_ in [((64, 33, 0), (320, 96, 200)),   # L % B != 0
+                   ((65, 32, 0), (320, 96, 200)),   # P_i > prompt_len
+                   ((64, 32, 0), (320, 96, 0))]:    # empty sequence
+        p = bd.Problem(3, 64, 320, 4, 4, 2, 128, seq_prompt_lens=P_, seq_response_lens=R_)
+        assert L.bd_attn_workspace_bytes(ctypes.byref(p.c()), 1) == 0
+        assert L.bd_packed_len(ctypes.byref(p.c())) == -1
+    half = bd.Problem(3, 64, 320, 4, 4, 2, 128, seq_prompt_lens=(64, 32, 0))
+    assert L.bd_packed_len(ctypes.byref(half.c())) == -1
