@@ -52,12 +52,15 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
                                                       const int* __restrict__ map, int map_stride) {
   constexpr int kTpr = D / 8;             // threads per row
   constexpr int kRows = 256 / kTpr;       // rows per block
-  const int bh = blockIdx.y;
-  const int b = bh / Hq, h = bh - b * Hq;
+  // varlen: blockIdx.y / Hq indexes the per-sequence maps, which name their
+  // sequence; rows past that sequence's packed length are padding
+  const int mi = blockIdx.y / Hq, h = blockIdx.y - mi * Hq;
+  const int* mapb = map + (size_t)mi * map_stride;
+  const int b = VARLEN ? map_seq(mapb) : mi;
+  const int bh = b * Hq + h;
   const int n = blockIdx.x * kRows + threadIdx.x / kTpr;
   const int sub = threadIdx.x % kTpr;
-  // varlen: rows past this sequence's packed length are padding
-  const Geom g = VARLEN ? map_geom(map + (size_t)b * map_stride) : gm;
+  const Geom g = VARLEN ? map_geom(mapb) : gm;
   const bool valid = n < (VARLEN ? g.N : N);
   float acc = 0.f;
   if (valid) {
@@ -257,9 +260,10 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
   // concurrently resident CTAs stream the same Q / dO tiles (L2 reuse).
   const int unit = blockIdx.x / gm.NT;
   const int rank = blockIdx.x - unit * gm.NT;
-  const int b = unit / a.n_kv_heads;
-  const int kvh = unit - b * a.n_kv_heads;
-  const int* mapb = VARLEN ? a.map + (size_t)b * a.map_stride : a.map;
+  const int mi = unit / a.n_kv_heads;  // map slot (varlen: longest sequences first)
+  const int kvh = unit - mi * a.n_kv_heads;
+  const int* mapb = VARLEN ? a.map + (size_t)mi * a.map_stride : a.map;
+  const int b = VARLEN ? map_seq(mapb) : mi;
   const Geom gsq = VARLEN ? map_geom(mapb) : gm;
   const Geom& g = VARLEN ? gsq : gm;
   if (VARLEN && rank >= g.NT) return;
@@ -592,10 +596,11 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
   const int unit = blockIdx.x / per_unit;
   const int rem = blockIdx.x - unit * per_unit;
   const int rank = rem / a.group;
-  const int b = unit / a.n_kv_heads;
-  const int kvh = unit - b * a.n_kv_heads;
+  const int mi = unit / a.n_kv_heads;  // map slot (varlen: longest sequences first)
+  const int kvh = unit - mi * a.n_kv_heads;
   const int h = kvh * a.group + (rem - rank * a.group);
-  const int* mapb = VARLEN ? a.map + (size_t)b * a.map_stride : a.map;
+  const int* mapb = VARLEN ? a.map + (size_t)mi * a.map_stride : a.map;
+  const int b = VARLEN ? map_seq(mapb) : mi;
   const Geom gsq = VARLEN ? map_geom(mapb) : gm;
   const Geom& g = VARLEN ? gsq : gm;
   if (VARLEN && rank >= g.NT) return;

@@ -166,11 +166,12 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
   const int unit = blockIdx.x / per_unit;
   const int rem = blockIdx.x - unit * per_unit;
   const int rank = rem / hp_per_kv;
-  const int b = unit / a.n_kv;
-  const int kvh = unit - b * a.n_kv;
+  const int mi = unit / a.n_kv;  // map slot (varlen: longest sequences first)
+  const int kvh = unit - mi * a.n_kv;
   const int h0 = kvh * a.group + (rem - rank * hp_per_kv) * NQ;
   // varlen: this sequence's own map and geometry; ranks past its tile count exit
-  const int* mapb = VARLEN ? a.map + (size_t)b * a.map_stride : a.map;
+  const int* mapb = VARLEN ? a.map + (size_t)mi * a.map_stride : a.map;
+  const int b = VARLEN ? map_seq(mapb) : mi;
   const Geom gsq = VARLEN ? map_geom(mapb) : gm;
   const Geom& g = VARLEN ? gsq : gm;
   if (VARLEN && rank >= g.NT) return;

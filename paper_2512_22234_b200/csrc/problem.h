@@ -1,5 +1,6 @@
 // Validation of bd_problem and derived geometry (host).
 #pragma once
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -61,9 +62,14 @@ inline SeqLens seq_lens_of(const bd_problem& p) {
   s.repeat_prompt = p.repeat_prompt;
   s.B = p.block_size;
   s.S = p.n_copies > 1 ? p.n_copies : 1;
+  for (int i = 0; i < p.batch; ++i) s.seq[i] = i;
+  // longest first (stable), see tilemap.cuh SeqLens
+  std::stable_sort(s.seq, s.seq + p.batch, [&](int a, int b) {
+    return p.seq_prompt_len[a] + p.seq_response_len[a] > p.seq_prompt_len[b] + p.seq_response_len[b];
+  });
   for (int i = 0; i < p.batch; ++i) {
-    s.P[i] = p.seq_prompt_len[i];
-    s.R[i] = p.seq_response_len[i];
+    s.P[i] = p.seq_prompt_len[s.seq[i]];
+    s.R[i] = p.seq_response_len[s.seq[i]];
   }
   return s;
 }

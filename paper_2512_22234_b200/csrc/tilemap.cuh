@@ -205,7 +205,7 @@ __host__ __device__ inline int entry_kind(int e) { return (e >> 28) & 0xF; }
 //   fwd_order[NT]  q-tiles by decreasing row length (longest first, LPT)
 //   bwd_order[NT]  k-tiles by decreasing column length
 constexpr int kMapMagic = 0x42444D31;  // "BDM1"
-constexpr int kMapHeader = 16;  // [8] = S (noisy copies); [9..15] reserved
+constexpr int kMapHeader = 16;  // [8] = S (noisy copies); [9] = sequence (varlen); [10..15] reserved
 
 struct MapView {
   int* base;
@@ -232,12 +232,18 @@ __host__ __device__ inline long long map_words(const Geom& g) {
 // Geometry of the sequence whose map starts at `base` (varlen batches keep
 // one map per sequence; the kernels read their sequence's geometry from it).
 __host__ __device__ inline Geom map_geom(const int* base) { return make_geom(base[1], base[2], base[3], base[8]); }
+__host__ __device__ inline int map_seq(const int* base) { return base[9]; }
 
 // Per-sequence lengths of a varlen batch, passed by
 // value to the map builder (kernel parameter: no host->device copy, no sync).
+// Entry i describes sequence seq[i]; the host lists the sequences longest
+// first, and map i is built for entry i, so the (sequence, kv head)-major
+// grid of the attention kernels starts the long sequences first (LPT across
+// the batch) while keeping each sequence's CTAs together (L2 reuse).
 constexpr int kMaxVarlenSeqs = 1024;
 struct SeqLens {
   int n, repeat_prompt, B, S;
+  int seq[kMaxVarlenSeqs];
   int P[kMaxVarlenSeqs];
   int R[kMaxVarlenSeqs];
 };

@@ -115,7 +115,7 @@ __device__ int classify_pair_warp(const Geom& g, int qt, int kt, const int* s_lo
 
 // One warp per q-tile (strided).  Shared memory: rowlen[NT], collen[NT],
 // colfill[NT], scan scratch[1024], and per warp 4 x 128 ints of row intervals.
-__device__ void build_map_body(const Geom& g, int* __restrict__ ws) {
+__device__ void build_map_body(const Geom& g, int* __restrict__ ws, int seq) {
   extern __shared__ int sh[];
   const int NT = g.NT;
   int* rowlen = sh;                 // NT
@@ -201,17 +201,18 @@ __device__ void build_map_body(const Geom& g, int* __restrict__ ws) {
     ws[6] = mv.row_ptr()[NT];
     ws[7] = maxrow;
     ws[8] = g.S;
+    ws[9] = seq;
   }
 }
 
 __global__ void __launch_bounds__(kBuildThreads, 1) build_map_kernel(Geom g, int* __restrict__ ws) {
-  build_map_body(g, ws);
+  build_map_body(g, ws, 0);
 }
 
 // Varlen: CTA i builds sequence i's map at ws + i * stride.
 __global__ void __launch_bounds__(kBuildThreads, 1)
     build_map_varlen_kernel(const __grid_constant__ SeqLens lens, int* __restrict__ ws, long long stride) {
-  build_map_body(seq_geom(lens, blockIdx.x), ws + blockIdx.x * stride);
+  build_map_body(seq_geom(lens, blockIdx.x), ws + blockIdx.x * stride, lens.seq[blockIdx.x]);
 }
 
 }  // namespace

@@ -81,8 +81,11 @@ class Problem:
 
     @staticmethod
     def from_cfg(cfg, **kw):
+        rl = getattr(cfg, "resp_lens", None)
         p = Problem(cfg.batch, cfg.prompt_len, cfg.response_len, cfg.block_size, cfg.n_q_heads,
-                    cfg.n_kv_heads, cfg.head_dim, cfg.repeat_prompt, n_copies=getattr(cfg, "n_copies", 1))
+                    cfg.n_kv_heads, cfg.head_dim, cfg.repeat_prompt, n_copies=getattr(cfg, "n_copies", 1),
+                    seq_prompt_lens=None if rl is None else (cfg.prompt_len,) * cfg.batch,
+                    seq_response_lens=None if rl is None else tuple(rl))
         return p.with_(**kw) if kw else p
 
 

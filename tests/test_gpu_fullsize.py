@@ -126,3 +126,38 @@ def test_fullsize_logprob_sampled(cuda_ok):
     ref_dz = olp.logprob_grad(z_rows, t[rows].long().cpu(), t2np(w[rows]).astype(np.float64))
     md = metrics(t2np(z[rows]), ref_dz)
     assert md["finite"] and md["rel_l2"] <= DZ_REL_L2, md
+
+
+@pytest.mark.gpu
+def test_fullsize_varlen_sampled(cuda_ok):
+    """sdar_8b_varlen (16 sequences, R_i ~ U[512, 8192]) in bench's launch
+    configuration: sampled rows of the shortest and the longest sequence vs
+    the oracle run on that sequence alone; padding rows untouched."""
+    cfg = CONFIGS["sdar_8b_varlen"]
+    prob = bd.Problem.from_cfg(cfg)
+    q, k, v, do = attn_inputs(cfg, device="cuda")
+    SENT = -3.0
+    o = torch.full_like(q, SENT)
+    lse = torch.full((cfg.batch, cfg.n_q_heads, cfg.ntot), SENT, device="cuda")
+    o, lse = bd.attn_fwd(prob, q, k, v, o, lse)
+    dq = torch.full_like(q, SENT)
+    dq, dk, dv = bd.attn_bwd(prob, q, k, v, o, lse, do, dq=dq)
+    torch.cuda.synchronize()
+    lens = list(cfg.resp_lens)
+    for b in (int(np.argmin(lens)), int(np.argmax(lens))):
+        R = lens[b]
+        n_b = prob.seq_packed_len(b)
+        one = OProblem(1, cfg.prompt_len, R, cfg.block_size, 1, 1, cfg.head_dim, cfg.repeat_prompt)
+        L = cfg.prompt_len + R
+        rows = np.unique(np.concatenate([[0, L - 1, L, n_b - 1], np.random.default_rng(b).integers(0, n_b, 64)]))
+        h = cfg.n_q_heads - 1
+        g_ = h // (cfg.n_q_heads // cfg.n_kv_heads)
+        qs, ks, vs, dos = (x[b:b + 1, :n_b, hh:hh + 1].float().cpu() for x, hh in ((q, h), (k, g_), (v, g_), (do, h)))
+        o_r, l_r = attention.forward_rows(one, qs, ks, vs, 0, 0, rows)
+        dq_r, _, _ = attention.backward_rows(one, qs, ks, vs, dos, 0, 0, rows)
+        mo = metrics(t2np(o[b, rows, h]), o_r)
+        assert mo["finite"] and mo["max_abs"] <= FWD_MAX_ABS and mo["rel_l2"] <= FWD_REL_L2, (b, mo)
+        assert metrics(t2np(lse[b, h, rows]), l_r)["max_abs"] <= FWD_MAX_ABS
+        mq = metrics(t2np(dq[b, rows, h]), dq_r)
+        assert mq["finite"] and mq["rel_l2"] <= GRAD_REL_L2, (b, mq)
+        assert torch.all(o[b, n_b:] == SENT) and torch.all(lse[b, :, n_b:] == SENT) and torch.all(dq[b, n_b:] == SENT)

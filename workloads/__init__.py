@@ -37,6 +37,7 @@ class AttnConfig:
     repeat_prompt: int = 1
     seed: int = 0
     n_copies: int = 1  # S noisy copies: trace replay (reading c19)
+    resp_lens: tuple = None  # varlen: per-sequence response lengths (<= response_len)
 
     @property
     def L(self):
@@ -67,6 +68,13 @@ CONFIGS = {
     # trace replay: SDAR-8B shape, B = 4 decoded one token
     # per step -> S = 4 noisy copies [x0 | xt(1) | .. | xt(4)], Ntot = 5 L
     "trace_s4": AttnConfig("trace_s4", 16, 32, 8, 128, 1024, 8192, 4, seed=5, n_copies=4),
+    # varlen: SDAR-8B heads, one group of 16 rollouts with
+    # response lengths ~ U[512, 8192] (multiples of B, seeded): mean ~4.3k, inside
+    # the paper's 707-5,434 per-benchmark averages under the 8k cap
+    "sdar_8b_varlen": AttnConfig("sdar_8b_varlen", 16, 32, 8, 128, 1024, 8192, 4, seed=6,
+                                 resp_lens=tuple(int(x) for x in (
+                                     (torch.randint(128, 2049, (16,), generator=torch.Generator().manual_seed(6))
+                                      * 4).tolist()))),
 }
 
 # logprob rows per config: N = b * R response rows
@@ -143,11 +151,27 @@ def useful_pairs(cfg: AttnConfig) -> int:
     return (1 + cfg.n_copies) * cfg.L * (cfg.L + cfg.block_size) // 2
 
 
+def total_pairs(cfg: AttnConfig) -> int:
+    """Visible pairs per head summed over the batch (varlen: per sequence)."""
+    if cfg.resp_lens is None:
+        return cfg.batch * useful_pairs(cfg)
+    return sum(useful_pairs(cfg.with_(response_len=r, resp_lens=None)) for r in cfg.resp_lens)
+
+
+def total_tokens(cfg: AttnConfig) -> int:
+    """Original (clean) tokens of the batch, sum of L_i."""
+    if cfg.resp_lens is None:
+        return cfg.batch * cfg.L
+    return sum(cfg.prompt_len + r for r in cfg.resp_lens)
+
+
 def useful_flops(cfg: AttnConfig, pairs=None):
     """(fwd, bwd) useful FLOPs: fwd = 4 d Hq b pairs, bwd = 2.5 x fwd
     (flash convention)."""
-    pairs = useful_pairs(cfg) if pairs is None else pairs
-    fwd = 4 * cfg.head_dim * cfg.n_q_heads * cfg.batch * pairs
+    if pairs is None:
+        fwd = 4 * cfg.head_dim * cfg.n_q_heads * total_pairs(cfg)
+    else:
+        fwd = 4 * cfg.head_dim * cfg.n_q_heads * cfg.batch * pairs
     return fwd, 2.5 * fwd
 
 
@@ -155,5 +179,6 @@ def _ceil_div(a, b):
     return -(-a // b)
 
 
-__all__ = ["AttnConfig", "CONFIGS", "attn_inputs", "logits_inputs", "rl_batch", "useful_pairs",
+__all__ = ["AttnConfig", "CONFIGS", "attn_inputs", "logits_inputs", "rl_batch", "useful_pairs", "total_pairs",
+           "total_tokens",
            "useful_flops", "VOCAB_QWEN3", "LOGPROB_ROWS", "math"]
