@@ -18,6 +18,8 @@ companion spec (``SPEC.md``, cited as ``S:<line>``):
 * ``dipo``      -- group advantages and the DiPO / DAPO token-level
                    reduction at the stop-gradient behaviour policy
                    (P:92, P:172-174, P:179-225; S:462-479).
+* ``lmhead``    -- LM head z = h W^T followed by the log-softmax gather, and
+                   its gradients dh, dW.
 * ``tilemap``   -- 128x128 tile classification computed *from the dense
                    mask* (FULL / PARTIAL / EMPTY), the definition the GPU
                    tile-map builder must match bit-exactly.
@@ -29,4 +31,4 @@ differences).  Parity status of each function is listed in DESIGN.md §3.
 """
 
 from .problem import Problem  # noqa: F401
-from . import mask, attention, logprob, dipo, tilemap  # noqa: F401
+from . import mask, attention, logprob, dipo, tilemap, lmhead  # noqa: F401

@@ -126,6 +126,25 @@ def logits_inputs(n_rows, vocab, device="cpu", seed=0, peaked=False, dtype=torch
     return z.to(dtype), t.to(torch.int32)
 
 
+# LM head + logprob: rows = b * R response rows,
+# hidden = [ext] Qwen3 hidden size (4,096 for 8B, 2,048 for 1.7B), V = 151,936.
+LMHEAD_SHAPES = {"tiny": (64, 256, 1000), "sdar_1_7b": (16 * 2048, 2048, VOCAB_QWEN3),
+                 "sdar_8b": (16 * 8192, 4096, VOCAB_QWEN3)}
+
+
+def lmhead_inputs(n_rows, hidden, vocab, device="cpu", seed=0, dtype=torch.bfloat16):
+    """h ~ N(0, 1) [n_rows, hidden] (post-final-norm hidden states), W ~ N(0, (3/sqrt(hidden))^2)
+    [vocab, hidden] (so logits ~ N(0, 3^2) like logits_inputs), uniform targets int32 [n_rows]
+    and upstream weights w ~ N(0, 1) fp32 [n_rows]."""
+    g = _gen(seed, device)
+    h = torch.randn((n_rows, hidden), generator=g, device=device, dtype=torch.float32).to(dtype)
+    W = (torch.randn((vocab, hidden), generator=g, device=device, dtype=torch.float32)
+         * (3.0 / math.sqrt(hidden))).to(dtype)
+    t = torch.randint(0, vocab, (n_rows,), generator=g, device=device, dtype=torch.int64).to(torch.int32)
+    w = torch.randn((n_rows,), generator=g, device=device, dtype=torch.float32)
+    return h, W, t, w
+
+
 def rl_batch(n_groups, group_size, resp_lens, seed=0):
     """Rewards ~ Bernoulli(0.5), trajectory/group ids and per-token traj ids.
 
@@ -179,6 +198,6 @@ def _ceil_div(a, b):
     return -(-a // b)
 
 
-__all__ = ["AttnConfig", "CONFIGS", "attn_inputs", "logits_inputs", "rl_batch", "useful_pairs", "total_pairs",
+__all__ = ["AttnConfig", "CONFIGS", "attn_inputs", "logits_inputs", "lmhead_inputs", "LMHEAD_SHAPES", "rl_batch", "useful_pairs", "total_pairs",
            "total_tokens",
            "useful_flops", "VOCAB_QWEN3", "LOGPROB_ROWS", "math"]
