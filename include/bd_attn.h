@@ -145,6 +145,41 @@ int bd_logprob(int64_t n_rows, int32_t vocab, const void* logits, int64_t row_st
 int bd_logprob_bwd(int64_t n_rows, int32_t vocab, const void* logits, int64_t row_stride, const int32_t* targets,
                    const float* lse, const float* dlogp, void* dlogits, int64_t dlogits_stride, void* stream);
 
+/* ---- LM head fused with the log-softmax gather ----
+ * The policy probabilities of Eqs. 6-8 are the softmax of the
+ * logits z = h W^T of the (bias-free, [ext] Qwen3/SDAR) LM head.  These calls
+ * compute log-probs and their gradients straight from the hidden states: the
+ * forward never materialises z [n, V]; the backward materialises only a chunk
+ * of dz = w (1[v = t] - softmax(z)) (bf16, chunk_rows x V, in the workspace).
+ *   h        bf16 [n_rows, hidden]     final hidden states of the scored rows
+ *   w        bf16 [vocab, hidden]      LM-head weight (nn.Linear layout)
+ *   targets  int32 [n_rows]            token ids (reading c9: rows are the caller's choice)
+ * hidden and vocab must be multiples of 8 (16-byte rows; Qwen3: 4096 / 2048
+ * and 151,936), else BD_ERR_UNSUPPORTED; pointers 16-byte aligned.
+ * tcgen05 CTA-pair GEMMs (256 x 256 tiles), fp32 accumulation and fp32
+ * softmax; deterministic. */
+
+/* Workspace bytes: forward (backward = 0) holds per-chunk softmax partials;
+ * backward holds one dz chunk of min(chunk_rows, n_rows) rows (chunk_rows
+ * <= 0 means all rows).  0 for invalid sizes. */
+size_t bd_lmhead_workspace_bytes(int64_t n_rows, int32_t hidden, int32_t vocab, int backward, int64_t chunk_rows);
+
+/* Forward: logp[n] = z[n, t_n] - LSE_n, LSE_n = ln sum_v exp z[n, v], z = h W^T.
+ *   logp  fp32 [n_rows] (written; NaN for a target outside [0, vocab))
+ *   lse   fp32 [n_rows] (written; may be NULL -- the backward needs it) */
+int bd_lmhead_logprob(int64_t n_rows, int32_t hidden, int32_t vocab, const void* h, const void* w,
+                      const int32_t* targets, float* logp, float* lse, void* ws, size_t ws_bytes, void* stream);
+
+/* Backward for upstream gradient dlogp (fp32 [n_rows]) given the forward's lse:
+ *   dz = dlogp_n (1[v = t_n] - exp(z[n, v] - lse_n))      (recomputed, per chunk)
+ *   dh bf16 [n_rows, hidden] = dz W                       (written)
+ *   dw fp32 [vocab, hidden]  = dz^T h                     (written; summed over all rows)
+ * Rows are processed in chunks of chunk_rows (<= 0: all at once); ws must hold
+ * bd_lmhead_workspace_bytes(n_rows, hidden, vocab, 1, chunk_rows) bytes. */
+int bd_lmhead_logprob_bwd(int64_t n_rows, int32_t hidden, int32_t vocab, const void* h, const void* w,
+                          const int32_t* targets, const float* lse, const float* dlogp, void* dh, float* dw,
+                          int64_t chunk_rows, void* ws, size_t ws_bytes, void* stream);
+
 /* DiPO, step 1: per-group partial statistics of the local trajectories.
  *   rewards        fp32 [n_traj]       r_i
  *   group_of_traj  int32 [n_traj]      global group id in [0, n_groups)
@@ -202,6 +237,12 @@ int64_t bd_launch_count(void);
  * (K-major) and smem-A (MN-major); all fp32 [128][128]. */
 int bd_selftest_mma(const void* a, const void* b, const void* v, float* c, float* o_ts, float* o_ss, float* o_mn,
                     void* stream);
+
+/* Self-test of the CTA-pair GEMM engine behind bd_lmhead_*: out fp32 [M][N] =
+ * sum_k A[m, k] B[n, k]; a is bf16 [M][K] (a_mn = 0) or [K][M] (a_mn = 1), b
+ * likewise; M, N, K multiples of 8. */
+int bd_selftest_gemm(int32_t M, int32_t N, int32_t K, const void* a, int a_mn, const void* b, int b_mn, float* out,
+                     void* stream);
 
 #ifdef __cplusplus
 }

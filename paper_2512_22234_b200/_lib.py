@@ -54,6 +54,10 @@ SIGNATURES = {
     "bd_error_string": (ctypes.c_char_p, [ctypes.c_int]),
     "bd_last_error": (ctypes.c_char_p, []),
     "bd_selftest_mma": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
+    "bd_lmhead_workspace_bytes": (_SZ, [_I64, _I32, _I32, ctypes.c_int, _I64]),
+    "bd_lmhead_logprob": (ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "bd_lmhead_logprob_bwd": (ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _SZ, _P]),
+    "bd_selftest_gemm": (ctypes.c_int, [_I32, _I32, _I32, _P, ctypes.c_int, _P, ctypes.c_int, _P, _P]),
 }
 
 _lib = None

@@ -48,19 +48,25 @@ def build(verbose=False, force=False):
             return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
     nvcc = _nvcc()
-    for s in srcs:
+
+    def compile_one(s):
         o = os.path.join(objdir, os.path.basename(s) + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-c", s, "-o", o]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        r = subprocess.run([nvcc, *NVCC_FLAGS, "-c", s, "-o", o], capture_output=True, text=True)
         log = r.stdout + r.stderr
-        if verbose or r.returncode:
-            sys.stderr.write(log)
-        if r.returncode:
-            raise RuntimeError(f"nvcc failed on {s}")
         with open(o + ".ptxas.txt", "w") as f:
             f.write(log)
+        return s, o, r.returncode, log
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, srcs))
+    objs = []
+    for s, o, rc, log in results:
+        if verbose or rc:
+            sys.stderr.write(log)
+        if rc:
+            raise RuntimeError(f"nvcc failed on {s}")
         objs.append(o)
     tmp = LIB + ".tmp"
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC", "-o", tmp,

@@ -250,6 +250,47 @@ def logprob_bwd(logits, targets, lse, dlogp, dlogits=None):
     return dlogits
 
 
+def lmhead_logprob(h, w, targets):
+    """bd_lmhead_logprob: (logp, lse) fp32 [n] of softmax(h w^T) at targets, logits never materialised."""
+    _need_cuda(h, w, targets)
+    n, C = h.shape
+    V = w.shape[0]
+    logp = torch.empty(n, dtype=torch.float32, device=h.device)
+    lse = torch.empty(n, dtype=torch.float32, device=h.device)
+    L = _lib.lib()
+    ws = workspace(L.bd_lmhead_workspace_bytes(n, C, V, 0, 0), h.device)
+    check(L.bd_lmhead_logprob(n, C, V, h.data_ptr(), w.data_ptr(), targets.data_ptr(), logp.data_ptr(),
+                              lse.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(h)), "bd_lmhead_logprob")
+    return logp, lse
+
+
+def lmhead_logprob_bwd(h, w, targets, lse, dlogp, chunk_rows=16384, dh=None, dw=None):
+    """bd_lmhead_logprob_bwd: (dh bf16 like h, dw fp32 [V, C]) for upstream dL/dlogp."""
+    _need_cuda(h, w, targets, lse, dlogp)
+    n, C = h.shape
+    V = w.shape[0]
+    dh = torch.empty_like(h) if dh is None else dh
+    dw = torch.empty((V, C), dtype=torch.float32, device=h.device) if dw is None else dw
+    L = _lib.lib()
+    ws = workspace(L.bd_lmhead_workspace_bytes(n, C, V, 1, chunk_rows), h.device)
+    check(L.bd_lmhead_logprob_bwd(n, C, V, h.data_ptr(), w.data_ptr(), targets.data_ptr(), lse.data_ptr(),
+                                  dlogp.data_ptr(), dh.data_ptr(), dw.data_ptr(), chunk_rows, ws.data_ptr(),
+                                  ws.numel(), _stream_ptr(h)), "bd_lmhead_logprob_bwd")
+    return dh, dw
+
+
+def selftest_gemm(a, b, a_mn=False, b_mn=False):
+    """bd_selftest_gemm: fp32 A B^T of the CTA-pair GEMM engine (operands K- or MN-major)."""
+    _need_cuda(a, b)
+    M = a.shape[1] if a_mn else a.shape[0]
+    K = a.shape[0] if a_mn else a.shape[1]
+    N = b.shape[1] if b_mn else b.shape[0]
+    out = torch.empty((M, N), dtype=torch.float32, device=a.device)
+    check(_lib.lib().bd_selftest_gemm(M, N, K, a.data_ptr(), int(a_mn), b.data_ptr(), int(b_mn), out.data_ptr(),
+                                      _stream_ptr(a)), "bd_selftest_gemm")
+    return out
+
+
 def launch_count() -> int:
     """Kernels enqueued by libbdattn.so so far (process-wide)."""
     return int(_lib.lib().bd_launch_count())
