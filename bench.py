@@ -265,6 +265,10 @@ def run_ours(args):
                "inputs": "q,k,v,dO,targets,rewards H2D from pinned host; DiPO loss partials D2H; logits are the "
                          "caller's LM-head output and stay device-resident"}
 
+    nxt = None
+    if not args.no_next:
+        nxt = {"lmhead_logprob": bench_lmhead(peaks, peak_src)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, target_s=args.cpu_seconds)
@@ -337,11 +341,54 @@ def run_ours(args):
         "gpu_launches_per_rank": int(launches),
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "next_rows": nxt,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bench_lmhead(peaks, peak_src, reps=3):
+    """SURVEY 8(f) NEXT #2, measured beside the step (not part of it): the fused
+    LM head + logprob at the SDAR-8B shape, 131,072 response rows x hidden 4,096
+    x V 151,936 (LMHEAD_SHAPES).  Useful FLOPs: fwd 2 n C V (logits never
+    materialised), bwd 3 x fwd (logit recompute, dh = dz W, dW = dz^T h).
+    CUDA events on the launching stream; median of `reps` after one warm-up."""
+    from paper_2512_22234_b200 import ops
+    from workloads import lmhead_inputs, LMHEAD_SHAPES
+    n, C, V = LMHEAD_SHAPES["sdar_8b"]
+    h, W, t, w = lmhead_inputs(n, C, V, device="cuda", seed=7)
+    dh, dw = torch.empty_like(h), torch.empty((V, C), dtype=torch.float32, device="cuda")
+    st = torch.cuda.current_stream()
+
+    def timed(fn):
+        fn()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(st)
+            fn()
+            e1.record(st)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    _, lse = ops.lmhead_logprob(h, W, t)
+    fwd_ms = timed(lambda: ops.lmhead_logprob(h, W, t))
+    bwd_ms = timed(lambda: ops.lmhead_logprob_bwd(h, W, t, lse, w, chunk_rows=16384, dh=dh, dw=dw))
+    F = 2.0 * n * C * V
+    peak = peaks["bf16_tflops_sustained"]
+    fa, ba = F / (fwd_ms * 1e-3) / 1e12, 3 * F / (bwd_ms * 1e-3) / 1e12
+    del h, W, t, w, dh, dw
+    torch.cuda.empty_cache()
+    return {"workload": f"lmhead_sdar_8b ({n} rows x hidden {C} x V {V})", "bound": "tensor", "unit": "TFLOP/s",
+            "fwd_ms": round(fwd_ms, 3), "fwd_achieved": round(fa, 1), "fwd_frac": round(fa / peak, 4),
+            "bwd_ms": round(bwd_ms, 3), "bwd_achieved": round(ba, 1), "bwd_frac": round(ba / peak, 4),
+            "peak": peak, "peak_kind": f"bf16 sustained ({peak_src})",
+            "algorithmic": "fwd 2 n C V, bwd 6 n C V useful FLOPs",
+            "logits_bytes_not_materialised": n * V * 2}
 
 
 def load_traffic():
@@ -441,6 +488,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-next", action="store_true", help="skip the SURVEY 8(f) next-row measurements")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-rows", type=int, default=512)
     args = ap.parse_args()
