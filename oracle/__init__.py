@@ -20,6 +20,9 @@ companion spec (``SPEC.md``, cited as ``S:<line>``):
                    (P:92, P:172-174, P:179-225; S:462-479).
 * ``lmhead``    -- LM head z = h W^T followed by the log-softmax gather, and
                    its gradients dh, dW.
+* ``decode``    -- blockwise KV-cache decode attention and the dynamic
+                   threshold token selection (P:62-83,
+                   P:312; S:201-205).
 * ``tilemap``   -- 128x128 tile classification computed *from the dense
                    mask* (FULL / PARTIAL / EMPTY), the definition the GPU
                    tile-map builder must match bit-exactly.
@@ -31,4 +34,4 @@ differences).  Parity status of each function is listed in DESIGN.md §3.
 """
 
 from .problem import Problem  # noqa: F401
-from . import mask, attention, logprob, dipo, tilemap, lmhead  # noqa: F401
+from . import mask, attention, logprob, dipo, tilemap, lmhead, decode  # noqa: F401

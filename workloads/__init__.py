@@ -145,6 +145,27 @@ def lmhead_inputs(n_rows, hidden, vocab, device="cpu", seed=0, dtype=torch.bfloa
     return h, W, t, w
 
 
+# Blockwise KV-cache decode: per GPU the 8xB200 RL step's
+# 128 rollouts (128 prompts x G 8 / 8 GPUs), SDAR-8B heads, B = 4, cache capacity
+# P + R = 9,216; mid-rollout cache lengths kv_len ~ U over block multiples in
+# [P + B, P + R] (the active block's keys are the last B).
+DECODE_SHAPES = {"tiny": dict(batch=3, block=4, n_q_heads=4, n_kv_heads=2, head_dim=64, cap=300),
+                 "sdar_8b": dict(batch=128, block=4, n_q_heads=32, n_kv_heads=8, head_dim=128, cap=9216)}
+
+
+def decode_inputs(batch, block, n_q_heads, n_kv_heads, head_dim, cap, device="cpu", seed=0, min_len=None,
+                  dtype=torch.bfloat16):
+    """q [b, B, Hq, d], k/v caches [b, cap, Hkv, d] ~ N(0, 1) bf16 and kv_len int32 [b]
+    (multiples of B in [max(B, min_len), cap])."""
+    g = _gen(seed, device)
+    q = torch.randn((batch, block, n_q_heads, head_dim), generator=g, device=device).to(dtype)
+    k = torch.randn((batch, cap, n_kv_heads, head_dim), generator=g, device=device).to(dtype)
+    v = torch.randn((batch, cap, n_kv_heads, head_dim), generator=g, device=device).to(dtype)
+    lo = max(1, (min_len or block) // block)
+    kv_len = (torch.randint(lo, cap // block + 1, (batch,), generator=_gen(seed + 1, "cpu")) * block).to(torch.int32)
+    return q, k, v, kv_len.to(device)
+
+
 def rl_batch(n_groups, group_size, resp_lens, seed=0):
     """Rewards ~ Bernoulli(0.5), trajectory/group ids and per-token traj ids.
 
@@ -198,6 +219,6 @@ def _ceil_div(a, b):
     return -(-a // b)
 
 
-__all__ = ["AttnConfig", "CONFIGS", "attn_inputs", "logits_inputs", "lmhead_inputs", "LMHEAD_SHAPES", "rl_batch", "useful_pairs", "total_pairs",
+__all__ = ["AttnConfig", "CONFIGS", "attn_inputs", "logits_inputs", "lmhead_inputs", "LMHEAD_SHAPES", "decode_inputs", "DECODE_SHAPES", "rl_batch", "useful_pairs", "total_pairs",
            "total_tokens",
            "useful_flops", "VOCAB_QWEN3", "LOGPROB_ROWS", "math"]
