@@ -180,6 +180,40 @@ int bd_lmhead_logprob_bwd(int64_t n_rows, int32_t hidden, int32_t vocab, const v
                           const int32_t* targets, const float* lse, const float* dlogp, void* dh, float* dw,
                           int64_t chunk_rows, void* ws, size_t ws_bytes, void* stream);
 
+/* ---- Blockwise KV-cache decoding for the rollout ----
+ * Blockwise dLLMs denoise the active block k conditioned on the clean history,
+ * p(b^k_0 | b^k_t, b^{<k}) (Eq. 2), which admits a KV cache;
+ * SPEC's inference mask: the active block sees every earlier block
+ * and itself bidirectionally.
+ *
+ * Attention of the active block's B query rows to the first kv_len[b] cached
+ * keys of each sequence (the caller has written the active block's own K/V at
+ * [kv_len - B, kv_len)); no mask inside that range.
+ *   q        bf16 [b, B, Hq, d]          k_cache, v_cache  bf16 [b, cap, Hkv, d]
+ *   kv_len   int32 [b] (device), B <= kv_len <= cap; cache rows >= kv_len may
+ *            hold anything (never read into the result)
+ *   o        bf16 [b, B, Hq, d] (written)     lse  fp32 [b, Hq, B] natural log (written)
+ * d must be 128 and B <= 32 (else BD_ERR_UNSUPPORTED); GQA kv(h) = h / (Hq/Hkv);
+ * softmax_scale <= 0 -> 1/sqrt(d).  Split-KV tcgen05 kernel + combine;
+ * deterministic.  ws: bd_decode_workspace_bytes(...) bytes (0 = invalid args). */
+size_t bd_decode_workspace_bytes(int32_t batch, int32_t block, int32_t n_q_heads, int32_t n_kv_heads,
+                                 int32_t head_dim, int32_t cap);
+int bd_decode_attn(int32_t batch, int32_t block, int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim,
+                   int32_t cap, float softmax_scale, const void* q, const void* k_cache, const void* v_cache,
+                   const int32_t* kv_len, void* o, float* lse, void* ws, size_t ws_bytes, void* stream);
+
+/* Dynamic decoding step ("decoding tokens whose top-1 probability
+ * exceeds 0.9 directly"; reading c20).
+ *   logits  bf16 [b, B, vocab]    masked  uint8 [b, B] (1 = still [MASK])
+ *   token   int32 [b, B]  argmax_v (lowest index among ties)        (written)
+ *   conf    fp32 [b, B]   softmax probability of that token (fp32)   (written)
+ *   commit  uint8 [b, B]  1 for every masked position with conf > threshold;
+ *           if a sequence has masked positions but none qualifies, its most
+ *           confident one (lowest position among ties); 0 elsewhere   (written)
+ * threshold >= 1 gives static one-token-per-step decoding. */
+int bd_decode_select(int32_t batch, int32_t block, int32_t vocab, const void* logits, const uint8_t* masked,
+                     float threshold, int32_t* token, float* conf, uint8_t* commit, void* stream);
+
 /* DiPO, step 1: per-group partial statistics of the local trajectories.
  *   rewards        fp32 [n_traj]       r_i
  *   group_of_traj  int32 [n_traj]      global group id in [0, n_groups)

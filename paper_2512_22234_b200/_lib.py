@@ -57,6 +57,9 @@ SIGNATURES = {
     "bd_lmhead_workspace_bytes": (_SZ, [_I64, _I32, _I32, ctypes.c_int, _I64]),
     "bd_lmhead_logprob": (ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "bd_lmhead_logprob_bwd": (ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _SZ, _P]),
+    "bd_decode_workspace_bytes": (_SZ, [_I32, _I32, _I32, _I32, _I32, _I32]),
+    "bd_decode_attn": (ctypes.c_int, [_I32, _I32, _I32, _I32, _I32, _I32, _F, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "bd_decode_select": (ctypes.c_int, [_I32, _I32, _I32, _P, _P, _F, _P, _P, _P, _P]),
     "bd_selftest_gemm": (ctypes.c_int, [_I32, _I32, _I32, _P, ctypes.c_int, _P, ctypes.c_int, _P, _P]),
 }
 

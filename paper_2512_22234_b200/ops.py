@@ -279,6 +279,35 @@ def lmhead_logprob_bwd(h, w, targets, lse, dlogp, chunk_rows=16384, dh=None, dw=
     return dh, dw
 
 
+def decode_attn(q, k_cache, v_cache, kv_len, softmax_scale=0.0, o=None, lse=None):
+    """bd_decode_attn: active-block attention over the KV cache -> (o bf16 like q, lse fp32 [b, Hq, B])."""
+    _need_cuda(q, k_cache, v_cache, kv_len)
+    b, B, Hq, d = q.shape
+    _, cap, Hkv, _ = k_cache.shape
+    o = torch.empty_like(q) if o is None else o
+    lse = torch.empty((b, Hq, B), dtype=torch.float32, device=q.device) if lse is None else lse
+    L = _lib.lib()
+    nbytes = L.bd_decode_workspace_bytes(b, B, Hq, Hkv, d, cap)
+    ws = workspace(max(nbytes, 256), q.device)
+    check(L.bd_decode_attn(b, B, Hq, Hkv, d, cap, float(softmax_scale), q.data_ptr(), k_cache.data_ptr(),
+                           v_cache.data_ptr(), kv_len.data_ptr(), o.data_ptr(), lse.data_ptr(), ws.data_ptr(),
+                           ws.numel(), _stream_ptr(q)), "bd_decode_attn")
+    return o, lse
+
+
+def decode_select(logits, masked, threshold=0.9):
+    """bd_decode_select over bf16 logits [b, B, V] and uint8 masked [b, B] -> (token, conf, commit)."""
+    _need_cuda(logits, masked)
+    b, B, V = logits.shape
+    token = torch.empty((b, B), dtype=torch.int32, device=logits.device)
+    conf = torch.empty((b, B), dtype=torch.float32, device=logits.device)
+    commit = torch.empty((b, B), dtype=torch.uint8, device=logits.device)
+    check(_lib.lib().bd_decode_select(b, B, V, logits.data_ptr(), masked.data_ptr(), float(threshold),
+                                      token.data_ptr(), conf.data_ptr(), commit.data_ptr(), _stream_ptr(logits)),
+          "bd_decode_select")
+    return token, conf, commit
+
+
 def selftest_gemm(a, b, a_mn=False, b_mn=False):
     """bd_selftest_gemm: fp32 A B^T of the CTA-pair GEMM engine (operands K- or MN-major)."""
     _need_cuda(a, b)

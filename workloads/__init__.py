@@ -149,7 +149,7 @@ def lmhead_inputs(n_rows, hidden, vocab, device="cpu", seed=0, dtype=torch.bfloa
 # 128 rollouts (128 prompts x G 8 / 8 GPUs), SDAR-8B heads, B = 4, cache capacity
 # P + R = 9,216; mid-rollout cache lengths kv_len ~ U over block multiples in
 # [P + B, P + R] (the active block's keys are the last B).
-DECODE_SHAPES = {"tiny": dict(batch=3, block=4, n_q_heads=4, n_kv_heads=2, head_dim=64, cap=300),
+DECODE_SHAPES = {"tiny": dict(batch=3, block=4, n_q_heads=4, n_kv_heads=2, head_dim=128, cap=300),
                  "sdar_8b": dict(batch=128, block=4, n_q_heads=32, n_kv_heads=8, head_dim=128, cap=9216)}
 
 
