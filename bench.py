@@ -267,7 +267,7 @@ def run_ours(args):
 
     nxt = None
     if not args.no_next:
-        nxt = {"lmhead_logprob": bench_lmhead(peaks, peak_src)}
+        nxt = {"lmhead_logprob": bench_lmhead(peaks, peak_src), "decode_attn": bench_decode(peaks, peak_src)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -389,6 +389,40 @@ def bench_lmhead(peaks, peak_src, reps=3):
             "peak": peak, "peak_kind": f"bf16 sustained ({peak_src})",
             "algorithmic": "fwd 2 n C V, bwd 6 n C V useful FLOPs",
             "logits_bytes_not_materialised": n * V * 2}
+
+
+def bench_decode(peaks, peak_src, reps=20):
+    """SURVEY 8(f) NEXT #4, measured beside the step: bd_decode_attn at the 8xB200
+    RL step's per-GPU rollout shape (128 sequences, SDAR-8B heads, B = 4, cache
+    capacity 9,216, kv_len ~ U[1,028, 9,216] in block multiples).  HBM-bound:
+    algorithmic bytes = cached K/V rows read (sum kv_len x Hkv x d x 4 B) + q + o.
+    L2 flushed (256 MB write) before each timed call; median of `reps`."""
+    from paper_2512_22234_b200 import ops
+    from workloads import decode_inputs, DECODE_SHAPES
+    sh = DECODE_SHAPES["sdar_8b"]
+    q, k, v, kv_len = decode_inputs(**sh, device="cuda", seed=21, min_len=1028)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+    o, lse = ops.decode_attn(q, k, v, kv_len)
+    ts = []
+    for i in range(reps + 3):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        ops.decode_attn(q, k, v, kv_len, o=o, lse=lse)
+        e1.record(st)
+        torch.cuda.synchronize()
+        if i >= 3:
+            ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    byts = int(kv_len.sum().item()) * sh["n_kv_heads"] * sh["head_dim"] * 4 + 2 * q.numel() * 2
+    gbs = byts / ms / 1e6
+    del q, k, v, flush
+    torch.cuda.empty_cache()
+    return {"workload": "decode_sdar_8b (128 seqs x Hq 32 / Hkv 8 x d 128, B 4, cap 9216)", "bound": "hbm",
+            "ms": round(ms, 4), "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(gbs / peaks["hbm_gbs"], 4), "peak_kind": f"HBM ({peak_src})",
+            "algorithmic_bytes": byts, "l2": "flushed before each call"}
 
 
 def load_traffic():
