@@ -277,9 +277,10 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
           if (q == NQ - 1) umma_commit(&kv_empty[slot(2 * j + 1)]);  // V(j) consumed
           if (has_next) {
             if (q == 0) mbar_wait(&kv_full[slot(2 * j + 2)], ph(2 * j + 2));
-            mbar_wait(&pv_done[q], j & 1);  // P_q(j) (aliasing S_q) consumed
+            // No wait for PV_q(j): tcgen05.mma ops of one thread execute in
+            // issue order, so S_q(j+1) overwrites the S/P columns only after
+            // PV_q(j) has read P_q(j) (WAR through the in-order tensor pipe).
             FTRACE(1024 + 8 * (j & 127) + 3 + q, blockIdx.x == 0);
-            tc_fence_after();
             issue_s(q, j + 1);
             if (q == NQ - 1) umma_commit(&kv_empty[slot(2 * j + 2)]);  // K(j+1) consumed
           }
