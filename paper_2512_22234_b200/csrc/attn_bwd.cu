@@ -401,7 +401,8 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
         if (has_next) {
           mbar_wait(&slot_full[slot_of(2 * i + 3)], phase_of(2 * i + 3));
           TRACE(1024 + 8 * (i & 127) + 4, blockIdx.x == 0);
-          mbar_wait(dv_done, i & 1);  // P^T(i) consumed -> dP^T columns free
+          // dV(i) reads P^T(i) from the dP^T columns; dP^T(i+1) may follow it
+          // at once (tcgen05.mma ops of one thread execute in issue order)
           TRACE(1024 + 8 * (i & 127) + 2, blockIdx.x == 0);
           tc_fence_after();
           issue_dp(i + 1);
@@ -722,7 +723,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         umma_commit(&kv_empty[slot(2 * j)]);  // K(j) consumed
         if (j + 2 < n_kt) {
           mbar_wait(&kv_full[slot(2 * j + 4)], ph(2 * j + 4));
-          mbar_wait(dq_done, j & 1);  // dS(j) in S[j&1] consumed
+          // dQ(j) reads dS(j) from S[j&1]; S(j+2) may follow it at once (in-order tensor pipe)
           TRACE(5120 + 8 * (j & 127) + 2, blockIdx.x == 0);
           tc_fence_after();
           issue_s(j + 2);
