@@ -45,8 +45,8 @@ struct FwdCfg {
   static constexpr int kOCol = 128 * NQ;          // O_q at kOCol + D q
   static constexpr int kTmemUsed = 128 * NQ + D * NQ;
   static constexpr uint32_t kTmemCols = kTmemUsed <= 256 ? 256 : 512;
-  // barriers: q_full, kv_full[S], kv_empty[S], s_full[NQ], p_full[NQ], pv_done[NQ]
-  static constexpr int kNumBars = 1 + 2 * kStages + 3 * NQ;
+  // barriers: q_full, kv_full[S], kv_empty[S], s_full[NQ], p_full[NQ], pv_done[NQ], p_half[NQ]
+  static constexpr int kNumBars = 1 + 2 * kStages + 4 * NQ;
   static constexpr int kSmemBytes = NQ * kTileBytes + kStages * kTileBytes + kNumBars * 8 + 16 + 1024;
 };
 
@@ -81,9 +81,9 @@ struct FwdArgs {
 #define BD_FWD_POLY_MOD 4
 #endif
 
-template <bool MASKED>
-__device__ __forceinline__ void softmax_tile(uint32_t tS, int lo, int hi, float sl2, float m, float& l,
-                                             float& m_new, bool& resc, float& alpha) {
+template <bool MASKED, int D>
+__device__ __forceinline__ void softmax_tile(uint32_t tS, uint32_t tO, int lo, int hi, float sl2, float m, float& l,
+                                             float& m_new, int j, uint64_t* p_half, int lane) {
   uint32_t sr[128];
 #pragma unroll
   for (int c = 0; c < 4; ++c) tmem_ld32(tS + 32 * c, sr + 32 * c);
@@ -106,13 +106,26 @@ __device__ __forceinline__ void softmax_tile(uint32_t tS, int lo, int hi, float 
                          fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
   const float tmax = mx * sl2;
   m_new = m;
-  resc = false;
+  bool resc = false;
   if (tmax > m + 8.f) {
     m_new = tmax;
     resc = true;
   }
   const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-  alpha = resc ? ex2_approx(m - m_use) : 1.f;
+  const float alpha = resc ? ex2_approx(m - m_use) : 1.f;
+  if (j > 0 && __any_sync(0xffffffffu, resc)) {
+    // O_q *= alpha before PV_q(j) accumulates into it (PV_q(j-1) has
+    // completed: S_q(j), issued after it, has completed)
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t ov[32];
+      tmem_ld32(tO + 32 * c, ov);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+      tmem_st32(tO + 32 * c, ov);
+    }
+  }
   const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_use, -m_use);
   float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
   uint32_t pk[64];
@@ -128,12 +141,20 @@ __device__ __forceinline__ void softmax_tile(uint32_t tS, int lo, int hi, float 
     }
     acc[c & 3] = fadd2(acc[c & 3], p);
     pk[c] = pack_bf16x2(p.x, p.y);
+    if (c == 47) {
+      // first 96 keys of P out: PV_q(j) k-steps 0-5 may start (p_half)
+      tmem_st32(tS, pk);
+      tmem_st16(tS + 32, pk + 32);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_half);
+    }
   }
   const float2 a01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
   const float sum = a01.x + a01.y;
   l = l * alpha + sum;
-#pragma unroll
-  for (int c = 0; c < 2; ++c) tmem_st32(tS + 32 * c, pk + 32 * c);
+  tmem_st16(tS + 48, pk + 48);
 }
 
 template <int D, int NQ, bool VARLEN>
@@ -152,6 +173,7 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
   uint64_t* s_full = kv_empty + C::kStages;
   uint64_t* p_full = s_full + NQ;
   uint64_t* pv_done = p_full + NQ;
+  uint64_t* p_half = pv_done + NQ;  // first 96 keys of P_q written
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
@@ -194,6 +216,7 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
       mbar_init(&s_full[q], 1);
       mbar_init(&p_full[q], 4);
       mbar_init(&pv_done[q], 1);
+      mbar_init(&p_half[q], 4);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmQ);
@@ -266,13 +289,21 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
         const bool has_next = j + 1 < n_kt;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
+          // PV_q(j) in two parts: keys 0-95 once P_q's first 96 columns are
+          // written (p_half), keys 96-127 at p_full -- overlaps the softmax tail
+          mbar_wait(&p_half[q], j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 6; ++k)
+            umma_ts(tbase + C::kOCol + D * q, tbase + C::kSCol + 128 * q + k * 8,
+                    umma_desc_sw128(vaddr + k * 2048, 16384, 1024), idesc_o, (j > 0 || k > 0) ? 1u : 0u);
           mbar_wait(&p_full[q], j & 1);
           FTRACE(1024 + 8 * (j & 127) + 1 + q, blockIdx.x == 0);
           tc_fence_after();
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
+          for (int k = 6; k < 8; ++k)
             umma_ts(tbase + C::kOCol + D * q, tbase + C::kSCol + 128 * q + k * 8,
-                    umma_desc_sw128(vaddr + k * 2048, 16384, 1024), idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+                    umma_desc_sw128(vaddr + k * 2048, 16384, 1024), idesc_o, 1u);
           umma_commit(&pv_done[q]);
           if (q == NQ - 1) umma_commit(&kv_empty[slot(2 * j + 1)]);  // V(j) consumed
           if (has_next) {
@@ -313,26 +344,13 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
       const bool xt = tile_seg(g, kt) != 0;
       const int lo = (xt ? lo1 : lo0) - k0;
       const int hi = min(xt ? hi1 : hi0, k1) - k0;
-      bool resc;
-      float alpha, m_new;
+      float m_new;
       // two separate code paths: the masked one must not be if-converted into
       // every tile (FULL tiles need no per-element work)
       if (need_mask)
-        softmax_tile<true>(tS, lo, hi, sl2, m, l, m_new, resc, alpha);
+        softmax_tile<true, D>(tS, tO, lo, hi, sl2, m, l, m_new, j, &p_half[q], lane);
       else
-        softmax_tile<false>(tS, lo, hi, sl2, m, l, m_new, resc, alpha);
-      if (j > 0 && __any_sync(0xffffffffu, resc)) {
-        // O_q *= alpha (PV(j-1) has completed: S_q(j) was issued after it)
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t ov[32];
-          tmem_ld32(tO + 32 * c, ov);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-          tmem_st32(tO + 32 * c, ov);
-        }
-      }
+        softmax_tile<false, D>(tS, tO, lo, hi, sl2, m, l, m_new, j, &p_half[q], lane);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
