@@ -195,14 +195,18 @@ __device__ __forceinline__ void p_row(const uint32_t* sr, float nlse2, float sl2
 // (a thread = one key row = one TMEM lane).  Per iteration i:
 //   phase 1 (needs S^T(i)):  P = exp2(S sl2 - lse2)          -> p1_done
 //   phase 2 (needs dP^T(i)): dS = P (dP - D); P^T (bf16) over the dP^T
-//            columns just read -> pt_done; dS^T to smem      -> ds_done
-//   MMA: S^T(i+1) at p1_done(i); dV(i) at pt_done(i); dK(i) at ds_done(i);
+//            columns just read, dS^T (bf16) beside it        -> pt_done
+//   MMA: S^T(i+1) at p1_done(i); dV(i), dK(i) at pt_done(i) (both TS: A = P^T /
+//        dS^T from TMEM);
 //        dP^T(i+1) once dV(i) has consumed P^T(i).
 // (dK(i) before dP^T(i+1) so that storing dS^T(i+1) never waits for dK(i).)
 template <int D>
 struct DkdvCfg {
   static constexpr int kTileBytes = 128 * D * 2;
-  static constexpr int kSlots = 4;
+  // dS^T lives in TMEM (next to P^T in the dP^T columns), so the 32 KB it
+  // took in smem buys a fifth Q/dO ring slot: loads are issued an iteration
+  // earlier and the dP^T(i+1) issue no longer waits for dO(i+1)
+  static constexpr int kSlots = 5;
   static constexpr int kWGs = 4;
   static constexpr int kCols = 128 / kWGs;  // q columns per warpgroup
   static constexpr int kComputeWarps = 4 * kWGs;
@@ -213,8 +217,7 @@ struct DkdvCfg {
   static constexpr uint32_t kTmemCols = 512;
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kTileBytes;
-  static constexpr int kOffDS = 2 * kTileBytes;
-  static constexpr int kOffRing = kOffDS + 128 * 128 * 2;
+  static constexpr int kOffRing = 2 * kTileBytes;
   static constexpr int kOffVec = kOffRing + kSlots * kTileBytes;
   static constexpr int kVecBytes = 2 * 128 * 4;
   static constexpr int kOffBar = kOffVec + 2 * kVecBytes;
@@ -234,7 +237,6 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sK = smem + C::kOffK;
   uint8_t* sV = smem + C::kOffV;
-  uint8_t* sDS = smem + C::kOffDS;
   uint8_t* sRing = smem + C::kOffRing;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* kv_full = bars;
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
     if (elect_one() && n_it > 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);  // S^T, dP^T
       constexpr uint32_t idesc_kv = umma_idesc_bf16(128, D, false, true);    // dV, dK: B MN-major
-      const uint32_t kaddr = smem_u32(sK), vaddr = smem_u32(sV), dsaddr = smem_u32(sDS);
+      const uint32_t kaddr = smem_u32(sK), vaddr = smem_u32(sV);
       auto ring = [&](int idx) { return smem_u32(sRing + slot_of(idx) * C::kTileBytes); };
       auto issue_s = [&](int i) {  // S^T = K Q^T
         const uint32_t qaddr = ring(2 * i);
@@ -388,12 +390,10 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
                   umma_desc_sw128(doaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
         umma_commit(dv_done);
         umma_commit(&slot_empty[slot_of(2 * i + 1)]);  // dO(i) consumed
-        mbar_wait(ds_done, i & 1);
         TRACE(1024 + 8 * (i & 127) + 3, blockIdx.x == 0);
-        tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < 8; ++k)  // dK += dS^T Q (A = dS^T smem K-major, B = Q MN-major)
-          umma_ss(tbase + C::kColDK, umma_desc_sw128(dsaddr + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024),
+        for (int k = 0; k < 8; ++k)  // dK += dS^T Q; dS^T (TMEM) of q block k at dP cols 32(k/2) + 16 + 8(k%2)
+          umma_ts(tbase + C::kColDK, tbase + C::kColDP + 32 * (k >> 1) + 16 + 8 * (k & 1),
                   umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
         TRACE(1024 + 8 * (i & 127) + 5, blockIdx.x == 0);
         umma_commit(dk_done);
@@ -474,27 +474,15 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
           pk[j] = pack_bf16x2(p0, p1);
         }
         tmem_st16(tP, pk);
+        tmem_st16(tP + 16, dsk);  // dS^T (bf16) beside P^T: the A operand of dK += dS^T Q
       }
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(pt_done);
+        mbar_arrive(pt_done);  // P^T(i) and dS^T(i) written: dV(i), dK(i) may be issued
         mbar_arrive(&vec_empty[i & 1]);
       }
-      // dS^T (bf16) into smem: K-major rows = keys; q columns [NC wg, +NC) are
-      // block (wg / 2), 16-byte chunks 4 (wg % 2) .. +3
-      if (i > 0) mbar_wait(dk_done, (i - 1) & 1);  // dK(i-1) has read dS^T(i-1)
-      {
-        uint8_t* dsrow = sDS + (wg >> 1) * 16384;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          *reinterpret_cast<uint4*>(dsrow + sw128_offset(r, (wg & 1) * 4 + u)) =
-              make_uint4(dsk[4 * u], dsk[4 * u + 1], dsk[4 * u + 2], dsk[4 * u + 3]);
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(ds_done);
       TRACE(8 * (i & 127) + 4, blockIdx.x == 0 && threadIdx.x == 0);
     }
     // ---- epilogue: dK (scaled), dV -> bf16; warpgroup wg stores columns [D/4 wg, +D/4)
