@@ -293,7 +293,9 @@ def run_ours(args):
 
     nxt = None
     if not args.no_next:
-        nxt = {"lmhead_logprob": bench_lmhead(peaks, peak_src), "decode_attn": bench_decode(peaks, peak_src)}
+        # decode first: measured right after the step, before the long LM-head GEMMs
+        dec = bench_decode(peaks, peak_src)
+        nxt = {"lmhead_logprob": bench_lmhead(peaks, peak_src), "decode_attn": dec}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
