@@ -388,7 +388,6 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
         for (int k = 0; k < 8; ++k)  // dV += P^T dO; P^T of q block k at dP cols 32(k/2) + 8(k%2)
           umma_ts(tbase + C::kColDV, tbase + C::kColDP + 32 * (k >> 1) + 8 * (k & 1),
                   umma_desc_sw128(doaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
-        umma_commit(dv_done);
         umma_commit(&slot_empty[slot_of(2 * i + 1)]);  // dO(i) consumed
         TRACE(1024 + 8 * (i & 127) + 3, blockIdx.x == 0);
 #pragma unroll
@@ -396,7 +395,6 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
           umma_ts(tbase + C::kColDK, tbase + C::kColDP + 32 * (k >> 1) + 16 + 8 * (k & 1),
                   umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
         TRACE(1024 + 8 * (i & 127) + 5, blockIdx.x == 0);
-        umma_commit(dk_done);
         umma_commit(&slot_empty[slot_of(2 * i)]);  // Q(i) consumed
         if (has_next) {
           mbar_wait(&slot_full[slot_of(2 * i + 3)], phase_of(2 * i + 3));
@@ -707,7 +705,6 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         for (int k = 0; k < 8; ++k)
           umma_ts(tbase + C::kColDQ, sbase + 32 * (k >> 1) + 8 * (k & 1),
                   umma_desc_sw128(kaddr + k * 2048, 16384, 1024), idesc_q, (j > 0 || k > 0) ? 1u : 0u);
-        umma_commit(dq_done);
         umma_commit(&kv_empty[slot(2 * j)]);  // K(j) consumed
         if (j + 2 < n_kt) {
           mbar_wait(&kv_full[slot(2 * j + 4)], ph(2 * j + 4));

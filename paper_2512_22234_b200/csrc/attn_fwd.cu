@@ -304,7 +304,9 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
           for (int k = 6; k < 8; ++k)
             umma_ts(tbase + C::kOCol + D * q, tbase + C::kSCol + 128 * q + k * 8,
                     umma_desc_sw128(vaddr + k * 2048, 16384, 1024), idesc_o, 1u);
-          umma_commit(&pv_done[q]);
+          // pv_done is observed only by the epilogue: commit the last tile only
+          // (no mbarrier phase completes unobserved; compute-sanitizer synccheck)
+          if (!has_next) umma_commit(&pv_done[q]);
           if (q == NQ - 1) umma_commit(&kv_empty[slot(2 * j + 1)]);  // V(j) consumed
           if (has_next) {
             if (q == 0) mbar_wait(&kv_full[slot(2 * j + 2)], ph(2 * j + 2));
@@ -359,7 +361,7 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
       m = m_new;
     }
     // ---- epilogue
-    mbar_wait(&pv_done[q], (n_kt - 1) & 1);
+    mbar_wait(&pv_done[q], 0);
     tc_fence_after();
     const int h = h0 + q;
     const bool valid = row < q1;
