@@ -314,6 +314,21 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
         tma_load_4d(sK + kb * 16384, &tmK, kv_full, kb * 64, kvh, k0, b);
         tma_load_4d(sV + kb * 16384, &tmV, kv_full, kb * 64, kvh, k0, b);
       }
+      // LSE / D vectors one iteration ahead of Q / dO: vec(i+1) is issued right
+      // after dO(i) (its 2-slot ring frees a whole iteration earlier than the
+      // Q / dO slots), so its ~1 us load latency is off the compute path
+      auto issue_vec = [&](int i) {
+        const int qt = entry_tile(ents[n_qt - 1 - i / a.group]);
+        const int h = kvh * a.group + (i % a.group);
+        const int vs = i & 1;
+        mbar_wait(&vec_empty[vs], ((i >> 1) & 1) ^ 1);
+        mbar_expect_tx(&vec_full[vs], C::kVecBytes);
+        const size_t vec = (((size_t)b * a.n_q_heads + h) * gm.NT + qt) * kTileRows;
+        float* sv = reinterpret_cast<float*>(smem + C::kOffVec + vs * C::kVecBytes);
+        bulk_load(sv, a.lse2_t + vec, 512, &vec_full[vs]);
+        bulk_load(sv + 128, a.dsum_t + vec, 512, &vec_full[vs]);
+      };
+      issue_vec(0);
       for (int i = 0; i < n_it; ++i) {
         const int qt = entry_tile(ents[n_qt - 1 - i / a.group]);  // decreasing q-tile: L2 reuse across CTAs
         const int h = kvh * a.group + (i % a.group);
@@ -327,13 +342,7 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
           for (int kb = 0; kb < D / 64; ++kb)
             tma_load_4d(sRing + s * C::kTileBytes + kb * 16384, w ? &tmDO : &tmQ, &slot_full[s], kb * 64, h, q0, b);
         }
-        const int vs = i & 1;
-        mbar_wait(&vec_empty[vs], ((i >> 1) & 1) ^ 1);
-        mbar_expect_tx(&vec_full[vs], C::kVecBytes);
-        const size_t vec = (((size_t)b * a.n_q_heads + h) * gm.NT + qt) * kTileRows;
-        float* sv = reinterpret_cast<float*>(smem + C::kOffVec + vs * C::kVecBytes);
-        bulk_load(sv, a.lse2_t + vec, 512, &vec_full[vs]);
-        bulk_load(sv + 128, a.dsum_t + vec, 512, &vec_full[vs]);
+        if (i + 1 < n_it) issue_vec(i + 1);
       }
     }
   } else if (warp == C::kMmaWarp) {

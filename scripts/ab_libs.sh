@@ -1,7 +1,9 @@
 #!/bin/bash
-# A/B timing of alternative builds of libbdattn.so (dev helper)
+# A/B timing of alternative builds of libbdattn.so (dev helper): each build timed twice, interleaved
+for rep in 1 2; do
 for L in scripts/libs_tmp/*.so; do
   cp "$L" paper_2512_22234_b200/libbdattn.so
   echo "== $L"
   PYTHONPATH=. timeout 200 python scripts/quick_attn.py ${1:-sdar_8b}
+done
 done
