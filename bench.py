@@ -111,13 +111,21 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ setup
-def dist_setup(gpus):
+def dist_setup(gpus, backend="nccl"):
+    """One process per GPU.  backend="gloo" with BD_BENCH_SHARE_GPU=1 maps every
+    rank onto cuda:0 -- a dry run of the multi-rank path on a 1-GPU box (NCCL
+    refuses two ranks on one GPU); never a scaling measurement."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        if os.environ.get("BD_BENCH_SHARE_GPU") == "1":
+            local = 0
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     if gpus != world and rank == 0:
@@ -201,7 +209,7 @@ class Step:
 
 
 def run_ours(args):
-    world, rank, local = dist_setup(args.gpus)
+    world, rank, local = dist_setup(args.gpus, args.dist_backend)
     cfg = CONFIGS[args.config]
     peaks, peak_src = load_peaks()
     step = Step(cfg, rank, world)
@@ -313,7 +321,7 @@ def run_ours(args):
     bwd_achieved = bwd_f / (phase["attn_bwd"] * 1e-3) / 1e12
     fwd_achieved = fwd_f / (phase["attn_fwd"] * 1e-3) / 1e12
     lp_bytes = step.n_rows * step.V * 2
-    traffic = load_traffic()
+    traffic = load_traffic() if cfg.name == "sdar_8b" else {}  # the ncu capture is at the SDAR-8B bench shape
     roofline = {"kernel": "bd_attn_bwd (attn_bwd_dkdv_kernel + attn_bwd_dq_kernel + bwd_pre + tile map)",
                 "bound": "tensor",
                 "achieved": round(bwd_achieved, 1), "peak": peak_s, "unit": "TFLOP/s",
@@ -551,6 +559,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the SURVEY 8(f) next-row measurements")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo + BD_BENCH_SHARE_GPU=1: multi-rank dry run on one GPU (not a measurement)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-rows", type=int, default=512)
     args = ap.parse_args()
