@@ -1,0 +1,33 @@
+"""The bench's multi-rank path (torchrun, one process per GPU, DiPO scalars
+all-reduced, max-over-ranks timing) run end to end as a 2-rank dry run on a
+single GPU: gloo backend, both ranks on cuda:0 (BD_BENCH_SHARE_GPU=1).  Checks
+the contract keys of the single JSON line rank 0 prints; the throughput of a
+shared-GPU run means nothing and is not checked."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_two_rank_dry_run(cuda_ok):
+    env = dict(os.environ, BD_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--steps", "2", "--warmup", "3", "--config", "tiny", "--dist-backend", "gloo", "--no-next",
+           "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 2 * d["config"]["batch_per_gpu"]
+    assert d["gpu_launches"] == 2 * d["gpu_launches_per_rank"] > 0
+    for key in ("metric", "value", "unit", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "roofline", "clocks", "e2e"):
+        assert key in d, key
