@@ -222,8 +222,8 @@ struct DkdvCfg {
   static constexpr int kVecBytes = 2 * 128 * 4;
   static constexpr int kOffBar = kOffVec + 2 * kVecBytes;
   // kv_full, slot_full[S], slot_empty[S], vec_full[2], vec_empty[2], s_full, dp_full, p1_done, pt_done,
-  // ds_done, dv_done, dk_done, acc_done
-  static constexpr int kNumBars = 1 + 2 * kSlots + 4 + 8;
+  // acc_done
+  static constexpr int kNumBars = 1 + 2 * kSlots + 4 + 5;
   static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16;
   static_assert(kSmemBytes <= 232448, "dkdv smem budget");
 };
@@ -248,10 +248,7 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
   uint64_t* dp_full = s_full + 1;
   uint64_t* p1_done = dp_full + 1;  // S^T(i) read
   uint64_t* pt_done = p1_done + 1;  // dP^T(i) read, P^T(i) written over it
-  uint64_t* ds_done = pt_done + 1;  // dS^T(i) in smem
-  uint64_t* dv_done = ds_done + 1;
-  uint64_t* dk_done = dv_done + 1;
-  uint64_t* acc_done = dk_done + 1;
+  uint64_t* acc_done = pt_done + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
@@ -295,9 +292,6 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
     mbar_init(dp_full, 1);
     mbar_init(p1_done, C::kComputeWarps);
     mbar_init(pt_done, C::kComputeWarps);
-    mbar_init(ds_done, C::kComputeWarps);
-    mbar_init(dv_done, 1);
-    mbar_init(dk_done, 1);
     mbar_init(acc_done, 1);
     fence_barrier_init();
   }
@@ -543,8 +537,8 @@ struct DqCfg {
   static constexpr int kOffDO = kTileBytes;
   static constexpr int kOffRing = 2 * kTileBytes;
   static constexpr int kOffBar = kOffRing + kStages * kTileBytes;
-  // q_full, kv_full[S], kv_empty[S], s_full[2], dp_full, dp_free, compute_done, dq_done, acc_done
-  static constexpr int kNumBars = 1 + 2 * kStages + 7;
+  // q_full, kv_full[S], kv_empty[S], s_full[2], dp_full, dp_free, compute_done, acc_done
+  static constexpr int kNumBars = 1 + 2 * kStages + 6;
   static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16;
 };
 
@@ -578,8 +572,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
   uint64_t* dp_full = s_full + 2;
   uint64_t* dp_free = dp_full + 1;       // compute has read dP(j)
   uint64_t* compute_done = dp_free + 1;  // dS(j) written over S[j&1]
-  uint64_t* dq_done = compute_done + 1;
-  uint64_t* acc_done = dq_done + 1;
+  uint64_t* acc_done = compute_done + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
@@ -620,7 +613,6 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
     mbar_init(dp_full, 1);
     mbar_init(dp_free, C::kComputeWarps);
     mbar_init(compute_done, C::kComputeWarps);
-    mbar_init(dq_done, 1);
     mbar_init(acc_done, 1);
     fence_barrier_init();
   }
