@@ -42,17 +42,21 @@ def build(verbose=False, force=False):
     srcs = sources()
     deps = srcs + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
         glob.glob(os.path.join(ROOT, "include", "*.h"))
-    if not force and os.path.exists(LIB):
+    if not force and not os.environ.get("BD_NVCC_EXTRA") and os.path.exists(LIB):
         lib_m = os.path.getmtime(LIB)
         if all(os.path.getmtime(d) <= lib_m for d in deps):
             return LIB
-    objdir = os.path.join(HERE, "build")
+    # dev A/B builds: extra nvcc flags (e.g. -DBD_DKDV_SPLIT=0) into a separate
+    # object dir and library path; the product build never sets these
+    extra = os.environ.get("BD_NVCC_EXTRA", "").split()
+    lib = os.environ.get("BD_LIB_OUT", LIB) if extra else LIB
+    objdir = os.path.join(HERE, "build" + ("_ab" if extra else ""))
     os.makedirs(objdir, exist_ok=True)
     nvcc = _nvcc()
 
     def compile_one(s):
         o = os.path.join(objdir, os.path.basename(s) + ".o")
-        r = subprocess.run([nvcc, *NVCC_FLAGS, "-c", s, "-o", o], capture_output=True, text=True)
+        r = subprocess.run([nvcc, *NVCC_FLAGS, *extra, "-c", s, "-o", o], capture_output=True, text=True)
         log = r.stdout + r.stderr
         with open(o + ".ptxas.txt", "w") as f:
             f.write(log)
@@ -68,15 +72,15 @@ def build(verbose=False, force=False):
         if rc:
             raise RuntimeError(f"nvcc failed on {s}")
         objs.append(o)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC", "-o", tmp,
            *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

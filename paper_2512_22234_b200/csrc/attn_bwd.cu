@@ -145,6 +145,9 @@ __device__ __forceinline__ void store_row_bf16_n(__nv_bfloat16* dst, const uint3
 #ifndef BD_DKDV_POLY_MOD
 #define BD_DKDV_POLY_MOD 0
 #endif
+#ifndef BD_DKDV_SPLIT
+#define BD_DKDV_SPLIT 1
+#endif
 #ifndef BD_DQ_POLY_MOD
 #define BD_DQ_POLY_MOD 0
 #endif
@@ -222,8 +225,8 @@ struct DkdvCfg {
   static constexpr int kVecBytes = 2 * 128 * 4;
   static constexpr int kOffBar = kOffVec + 2 * kVecBytes;
   // kv_full, slot_full[S], slot_empty[S], vec_full[2], vec_empty[2], s_full, dp_full, p1_done, pt_done,
-  // acc_done
-  static constexpr int kNumBars = 1 + 2 * kSlots + 4 + 5;
+  // acc_done, pt_half
+  static constexpr int kNumBars = 1 + 2 * kSlots + 4 + 6;
   static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16;
   static_assert(kSmemBytes <= 232448, "dkdv smem budget");
 };
@@ -249,6 +252,7 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
   uint64_t* p1_done = dp_full + 1;  // S^T(i) read
   uint64_t* pt_done = p1_done + 1;  // dP^T(i) read, P^T(i) written over it
   uint64_t* acc_done = pt_done + 1;
+  uint64_t* pt_half = acc_done + 1;  // first 16 q columns of every warpgroup: P^T, dS^T written
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
@@ -293,6 +297,7 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
     mbar_init(p1_done, C::kComputeWarps);
     mbar_init(pt_done, C::kComputeWarps);
     mbar_init(acc_done, 1);
+    mbar_init(pt_half, C::kComputeWarps);
     fence_barrier_init();
   }
   tc_fence_before();
@@ -384,6 +389,34 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
           tc_fence_after();
           issue_s(i + 1);
         }
+#if BD_DKDV_SPLIT
+        // P^T / dS^T arrive in two halves (q columns 0-15 and 16-31 of every
+        // warpgroup = the even and odd k-steps): the even k-steps of dV(i) and
+        // dK(i) run while the compute warps finish the odd half
+        mbar_wait(pt_half, i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; k += 2)
+          umma_ts(tbase + C::kColDV, tbase + C::kColDP + 32 * (k >> 1), umma_desc_sw128(doaddr + k * 2048, 16384, 1024),
+                  idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
+#pragma unroll
+        for (int k = 0; k < 8; k += 2)
+          umma_ts(tbase + C::kColDK, tbase + C::kColDP + 32 * (k >> 1) + 16,
+                  umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
+        mbar_wait(pt_done, i & 1);
+        TRACE(1024 + 8 * (i & 127) + 1, blockIdx.x == 0);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 1; k < 8; k += 2)
+          umma_ts(tbase + C::kColDV, tbase + C::kColDP + 32 * (k >> 1) + 8, umma_desc_sw128(doaddr + k * 2048, 16384, 1024),
+                  idesc_kv, 1u);
+        umma_commit(&slot_empty[slot_of(2 * i + 1)]);  // dO(i) consumed
+#pragma unroll
+        for (int k = 1; k < 8; k += 2)
+          umma_ts(tbase + C::kColDK, tbase + C::kColDP + 32 * (k >> 1) + 24,
+                  umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, 1u);
+        TRACE(1024 + 8 * (i & 127) + 5, blockIdx.x == 0);
+#else
         mbar_wait(pt_done, i & 1);
         TRACE(1024 + 8 * (i & 127) + 1, blockIdx.x == 0);
         tc_fence_after();
@@ -398,6 +431,7 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
           umma_ts(tbase + C::kColDK, tbase + C::kColDP + 32 * (k >> 1) + 16 + 8 * (k & 1),
                   umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
         TRACE(1024 + 8 * (i & 127) + 5, blockIdx.x == 0);
+#endif
         umma_commit(&slot_empty[slot_of(2 * i)]);  // Q(i) consumed
         if (has_next) {
           mbar_wait(&slot_full[slot_of(2 * i + 3)], phase_of(2 * i + 3));
@@ -465,6 +499,29 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
         tmem_ld32(tP, dr);
         tmem_ld_wait();
         uint32_t pk[NC / 2];
+#if BD_DKDV_SPLIT
+        static_assert(NC == 32, "split P^T arrival assumes 32 q columns per warpgroup");
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+          for (int j = 8 * hh; j < 8 * hh + 8; ++j) {
+            const float p0 = pv[2 * j], p1 = pv[2 * j + 1];
+            const float2 ds = fmul2(make_float2(p0, p1),
+                                    fadd2(make_float2(__uint_as_float(dr[2 * j]), __uint_as_float(dr[2 * j + 1])),
+                                          make_float2(sv[128 + 2 * j], sv[128 + 2 * j + 1])));  // sv = -D
+            dsk[j] = pack_bf16x2(ds.x, ds.y);
+            pk[j] = pack_bf16x2(p0, p1);
+          }
+          tmem_st8(tP + 8 * hh, pk + 8 * hh);
+          tmem_st8(tP + 16 + 8 * hh, dsk + 8 * hh);  // dS^T (bf16) beside P^T: A of dK += dS^T Q
+          if (hh == 0) {
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(pt_half);
+          }
+        }
+#else
 #pragma unroll
         for (int j = 0; j < NC / 2; ++j) {
           const float p0 = pv[2 * j], p1 = pv[2 * j + 1];
@@ -476,6 +533,7 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
         }
         tmem_st16(tP, pk);
         tmem_st16(tP + 16, dsk);  // dS^T (bf16) beside P^T: the A operand of dK += dS^T Q
+#endif
       }
       tmem_st_wait();
       tc_fence_before();
