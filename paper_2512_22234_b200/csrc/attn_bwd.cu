@@ -316,9 +316,10 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
       // LSE / D vectors one iteration ahead of Q / dO: vec(i+1) is issued right
       // after dO(i) (its 2-slot ring frees a whole iteration earlier than the
       // Q / dO slots), so its ~1 us load latency is off the compute path
-      auto issue_vec = [&](int i) {
-        const int qt = entry_tile(ents[n_qt - 1 - i / a.group]);
-        const int h = kvh * a.group + (i % a.group);
+      // iteration i = (column entry n_qt - 1 - i / group, head i % group), walked
+      // with counters (no integer division on the issue path)
+      auto issue_vec = [&](int i, int qt, int hs) {
+        const int h = kvh * a.group + hs;
         const int vs = i & 1;
         mbar_wait(&vec_empty[vs], ((i >> 1) & 1) ^ 1);
         mbar_expect_tx(&vec_full[vs], C::kVecBytes);
@@ -327,10 +328,10 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
         bulk_load(sv, a.lse2_t + vec, 512, &vec_full[vs]);
         bulk_load(sv + 128, a.dsum_t + vec, 512, &vec_full[vs]);
       };
-      issue_vec(0);
+      int eidx = n_qt - 1, qt = entry_tile(ents[eidx]), hs = 0;  // iteration i
+      issue_vec(0, qt, 0);
       for (int i = 0; i < n_it; ++i) {
-        const int qt = entry_tile(ents[n_qt - 1 - i / a.group]);  // decreasing q-tile: L2 reuse across CTAs
-        const int h = kvh * a.group + (i % a.group);
+        const int h = kvh * a.group + hs;  // decreasing q-tile: L2 reuse across CTAs
         const int q0 = tile_start(g, qt);
 #pragma unroll
         for (int w = 0; w < 2; ++w) {  // w = 0: Q(i), w = 1: dO(i)
@@ -341,7 +342,11 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
           for (int kb = 0; kb < D / 64; ++kb)
             tma_load_4d(sRing + s * C::kTileBytes + kb * 16384, w ? &tmDO : &tmQ, &slot_full[s], kb * 64, h, q0, b);
         }
-        if (i + 1 < n_it) issue_vec(i + 1);
+        if (++hs == a.group) {
+          hs = 0;
+          if (i + 1 < n_it) qt = entry_tile(ents[--eidx]);
+        }
+        if (i + 1 < n_it) issue_vec(i + 1, qt, hs);
       }
     }
   } else if (warp == C::kMmaWarp) {
@@ -455,8 +460,16 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
     const int kpos = k0 + r;
     const uint32_t tS = tbase + lane_off + C::kColS + wg * NC;
     const uint32_t tP = tbase + lane_off + C::kColDP + wg * NC;
+    // column entries walked with counters, the next q-tile's entry loaded a
+    // whole q-tile ahead (its global-load latency stays off the compute path)
+    int hs = 0, eidx = n_qt - 1;
+    int ent_next = n_it > 0 ? ents[eidx] : 0;
     for (int i = 0; i < n_it; ++i) {
-      const int ent = ents[n_qt - 1 - i / a.group];
+      const int ent = ent_next;
+      if (++hs == a.group) {
+        hs = 0;
+        if (--eidx >= 0) ent_next = ents[eidx];
+      }
       const int qt = entry_tile(ent);
       int q0, q1, qseg;
       tile_bounds(g, qt, q0, q1, qseg);
@@ -788,8 +801,10 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
     const size_t vslot = (((size_t)b * a.n_q_heads + h) * gm.NT + qt) * kTileRows + r;
     const float nlse2 = a.lse2_t[vslot];  // -lse2 and -D (negated by bwd_pre)
     const float ndsum = a.dsum_t[vslot];
+    int ent_next = n_kt > 0 ? ents[0] : 0;  // row entries loaded one tile ahead
     for (int j = 0; j < n_kt; ++j) {
-      const int ent = ents[j];
+      const int ent = ent_next;
+      if (j + 1 < n_kt) ent_next = ents[j + 1];
       const int kt = entry_tile(ent);
       const int k0 = tile_start(g, kt), k1 = tile_end(g, kt);
       const bool need_mask = entry_kind(ent) == kKindPartial || (k1 - k0) < 128;

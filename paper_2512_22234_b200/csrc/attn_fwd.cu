@@ -334,8 +334,10 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
     const float sl2 = a.scale_log2;
     float m = -INFINITY, l = 0.f;
 
+    int ent_next = n_kt > 0 ? ents[0] : 0;  // row entries loaded one tile ahead
     for (int j = 0; j < n_kt; ++j) {
-      const int ent = ents[j];
+      const int ent = ent_next;
+      if (j + 1 < n_kt) ent_next = ents[j + 1];
       const int kt = entry_tile(ent);
       const int k0 = tile_start(g, kt), k1 = tile_end(g, kt);
       const bool need_mask = entry_kind(ent) == kKindPartial || (k1 - k0) < 128;
