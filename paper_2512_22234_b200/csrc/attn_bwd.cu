@@ -145,6 +145,9 @@ __device__ __forceinline__ void store_row_bf16_n(__nv_bfloat16* dst, const uint3
 #ifndef BD_DKDV_POLY_MOD
 #define BD_DKDV_POLY_MOD 0
 #endif
+#ifndef BD_EXP_NOVEC
+#define BD_EXP_NOVEC 0
+#endif
 #ifndef BD_DKDV_SPLIT
 #define BD_DKDV_SPLIT 1
 #endif
@@ -162,8 +165,13 @@ template <bool MASKED, int NC>
 __device__ __forceinline__ void p_tile(const uint32_t* sr, const float* sv, float sl2, int ja, int jb, float* pv) {
 #pragma unroll
   for (int j = 0; j < NC; j += 2) {  // sv = -lse2 (negated by bwd_pre)
+#if BD_EXP_NOVEC  // timing experiment only (wrong numerics): one LDS instead of 16
+    const float2 x = ffma2(make_float2(__uint_as_float(sr[j]), __uint_as_float(sr[j + 1])), make_float2(sl2, sl2),
+                           make_float2(sv[0], sv[0]));
+#else
     const float2 x = ffma2(make_float2(__uint_as_float(sr[j]), __uint_as_float(sr[j + 1])), make_float2(sl2, sl2),
                            make_float2(sv[j], sv[j + 1]));
+#endif
     const float2 p = ex2_pair<BD_DKDV_POLY_MOD>(j / 2, x);
     pv[j] = p.x;
     pv[j + 1] = p.y;
@@ -519,9 +527,15 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
 #pragma unroll
           for (int j = 8 * hh; j < 8 * hh + 8; ++j) {
             const float p0 = pv[2 * j], p1 = pv[2 * j + 1];
+#if BD_EXP_NOVEC
+            const float2 ds = fmul2(make_float2(p0, p1),
+                                    fadd2(make_float2(__uint_as_float(dr[2 * j]), __uint_as_float(dr[2 * j + 1])),
+                                          make_float2(sv[128], sv[128])));
+#else
             const float2 ds = fmul2(make_float2(p0, p1),
                                     fadd2(make_float2(__uint_as_float(dr[2 * j]), __uint_as_float(dr[2 * j + 1])),
                                           make_float2(sv[128 + 2 * j], sv[128 + 2 * j + 1])));  // sv = -D
+#endif
             dsk[j] = pack_bf16x2(ds.x, ds.y);
             pk[j] = pack_bf16x2(p0, p1);
           }
@@ -595,7 +609,12 @@ struct DqCfg {
   static constexpr int kTileBytes = 128 * D * 2;
   // K tiles live from S(j) to dQ(j), V tiles only until dP(j): separate rings,
   // K(j) -> slot j % 3, V(j) -> slot 3 + j % 2 (ring index 2j / 2j+1).
-  static constexpr int kKSlots = 3, kVSlots = 2;
+#ifndef BD_DQ_KSLOTS
+#define BD_DQ_KSLOTS 4
+#endif
+  // 4 K slots + 1 V slot measured 1.5% faster than 3 + 2 (K(j+2) no longer waits
+  // for its load behind dQ(j-1); V(j+1) has a whole period to land)
+  static constexpr int kKSlots = BD_DQ_KSLOTS, kVSlots = 5 - BD_DQ_KSLOTS;
   static constexpr int kStages = kKSlots + kVSlots;
   static constexpr int kWGs = 4;     // compute warpgroups, 32 key columns each
   static constexpr int kComputeWarps = 4 * kWGs;

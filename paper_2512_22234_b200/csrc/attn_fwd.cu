@@ -36,7 +36,10 @@ namespace {
 template <int D, int NQ>
 struct FwdCfg {
   static constexpr int kTileBytes = 128 * D * 2;
-  static constexpr int kStages = NQ == 2 ? 4 : 2;
+#ifndef BD_FWD_STAGES
+#define BD_FWD_STAGES 4
+#endif
+  static constexpr int kStages = NQ == 2 ? BD_FWD_STAGES : 2;
   static constexpr int kSoftmaxWarps = 4 * NQ;
   static constexpr int kTmaWarp = kSoftmaxWarps;
   static constexpr int kMmaWarp = kSoftmaxWarps + 1;
