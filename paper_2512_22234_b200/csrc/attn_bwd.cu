@@ -894,6 +894,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
   if (warp == 0) tmem_dealloc<C::kTmemCols>(tbase);
 }
 
+
 template <typename K>
 int set_smem(K kernel, int bytes, bool& done) {
   if (done) return BD_OK;
