@@ -220,6 +220,9 @@ __global__ void __launch_bounds__(kThreads) logprob_bwd_kernel(int64_t n_rows, i
 // one HBM write of the logits (the two-kernel path reads them twice).
 // Requires V % (8 kCl) == 0 and 16-byte aligned rows (Qwen3 V = 151,936 is).
 constexpr int kCl = 4;
+#ifndef BD_LP_PACKED
+#define BD_LP_PACKED 1
+#endif
 constexpr int kFusedThreads = 256;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -291,6 +294,18 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
   // pass 1: max of the slice
   const int nv = Vc / 8;
   float mx = -INFINITY;
+#if BD_LP_PACKED
+  {  // packed bf16x2 max (exact): one HMNMX2 per two elements, no unpacking
+    __nv_bfloat162 m2v = __float2bfloat162_rn(-INFINITY);
+    for (int i = tid; i < nv; i += kFusedThreads) {
+      const uint4 u = buf4[i];
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) m2v = __hmax2(m2v, *reinterpret_cast<const __nv_bfloat162*>(&w[j]));
+    }
+    mx = fmaxf(__low2float(m2v), __high2float(m2v));
+  }
+#else
   for (int i = tid; i < nv; i += kFusedThreads) {
     const uint4 u = buf4[i];
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
@@ -298,6 +313,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
     for (int j = 0; j < 4; ++j)
       mx = fmaxf(mx, fmaxf(__uint_as_float(w[j] << 16), __uint_as_float(w[j] & 0xFFFF0000u)));
   }
+#endif
   mx = block_reduce(mx, red, true);
   if (tid == 0) part[0] = mx;
   cluster_sync_all();
@@ -306,6 +322,26 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
   const float m2 = m * kLog2e;
   // pass 2: e = 2^(x log2e - m2) stored over the slice (bf16), partial sum
   float sum = 0.f;
+#if BD_LP_PACKED
+  {  // packed fp32x2 argument (FFMA2) and sum (FADD2)
+    const float2 l2e = make_float2(kLog2e, kLog2e), nm2 = make_float2(-m2, -m2);
+    float2 acc = make_float2(0.f, 0.f);
+    for (int i = tid; i < nv; i += kFusedThreads) {
+      const uint4 u = buf4[i];
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 x = ffma2(make_float2(__uint_as_float(w[j] << 16), __uint_as_float(w[j] & 0xFFFF0000u)), l2e, nm2);
+        const float2 e = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+        acc = fadd2(acc, e);
+        o[j] = pack_bf16x2(e.x, e.y);
+      }
+      buf4[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    sum = acc.x + acc.y;
+  }
+#else
   for (int i = tid; i < nv; i += kFusedThreads) {
     const uint4 u = buf4[i];
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
@@ -319,6 +355,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
     }
     buf4[i] = make_uint4(o[0], o[1], o[2], o[3]);
   }
+#endif
   sum = block_reduce(sum, red, false);
   if (tid == 0) part[1] = sum;
   cluster_sync_all();
@@ -338,6 +375,39 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
   const float wgt = dlogp[row];
   const float scl = wgt / tot;
   uint4* out = reinterpret_cast<uint4*>(dz + row * dz_stride + (int64_t)crank * Vc);
+#if BD_LP_PACKED
+  {
+    // -scl e in packed bf16x2 arithmetic: -scl = hi + lo (two bf16), dz =
+    // fma(e, hi, e lo) rounds once, to within 2^-17 of bf16(-scl e); the one
+    // vector holding the target takes the fp32 path below
+    const float nscl = -scl;
+    const __nv_bfloat16 hi = __float2bfloat16_rn(nscl);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(nscl - __bfloat162float(hi));
+    const __nv_bfloat162 hi2 = __halves2bfloat162(hi, hi), lo2 = __halves2bfloat162(lo, lo);
+    const int tv = (tl >= 0 && tl < Vc) ? tl >> 3 : -1;
+    for (int i = tid; i < nv; i += kFusedThreads) {
+      const uint4 u = buf4[i];
+      uint32_t w[4] = {u.x, u.y, u.z, u.w};
+      if (i != tv) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const __nv_bfloat162 e2 = *reinterpret_cast<const __nv_bfloat162*>(&w[j]);
+          const __nv_bfloat162 d2 = __hfma2(e2, hi2, __hmul2(e2, lo2));
+          w[j] = *reinterpret_cast<const uint32_t*>(&d2);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int v0 = 8 * i + 2 * j;
+          const float g0 = (v0 == tl ? wgt : 0.f) - scl * __uint_as_float(w[j] << 16);
+          const float g1 = (v0 + 1 == tl ? wgt : 0.f) - scl * __uint_as_float(w[j] & 0xFFFF0000u);
+          w[j] = pack_bf16x2(g0, g1);
+        }
+      }
+      out[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+#else
   for (int i = tid; i < nv; i += kFusedThreads) {
     const uint4 u = buf4[i];
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
@@ -351,6 +421,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
     }
     out[i] = make_uint4(o[0], o[1], o[2], o[3]);
   }
+#endif
 }
 
 }  // namespace
