@@ -95,9 +95,22 @@ __global__ void zero_kernel(float4* __restrict__ p, size_t n4) {
 // stamps of its pipeline hand-offs into a static device buffer, read back by
 // bd_debug_trace().  Off by default (a warp-uniform predicate per event).
 __device__ long long g_trace[8192];
+// BD_TRACE=2: per-CTA timeline of the dQ kernel (globaltimer ns at entry and
+// exit, tile count, SM id) for the first 32768 CTAs, read by bd_debug_cta_timeline()
+__device__ long long g_cta_tl[4 * 32768];
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int smid() {
+  int r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 #define TRACE(slot, cond)                                         \
   do {                                                            \
-    if (a.trace && (cond)) g_trace[(slot)] = clock64();           \
+    if (a.trace == 1 && (cond)) g_trace[(slot)] = clock64();      \
   } while (0)
 
 struct BwdArgs {
@@ -147,6 +160,9 @@ __device__ __forceinline__ void store_row_bf16_n(__nv_bfloat16* dst, const uint3
 #endif
 #ifndef BD_EXP_NOVEC
 #define BD_EXP_NOVEC 0
+#endif
+#ifndef BD_DQ_PERSIST
+#define BD_DQ_PERSIST 1
 #endif
 #ifndef BD_DKDV_SPLIT
 #define BD_DKDV_SPLIT 1
@@ -628,7 +644,8 @@ struct DqCfg {
   static constexpr int kOffRing = 2 * kTileBytes;
   static constexpr int kOffBar = kOffRing + kStages * kTileBytes;
   // q_full, kv_full[S], kv_empty[S], s_full[2], dp_full, dp_free, compute_done, acc_done
-  static constexpr int kNumBars = 1 + 2 * kStages + 6;
+  // (+ qdo_empty, acc_empty in the persistent kernel)
+  static constexpr int kNumBars = 1 + 2 * kStages + 8;
   static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16;
 };
 
@@ -650,6 +667,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                        const BwdArgs a) {
   using C = DqCfg<D>;
+  const long long t_entry = (a.trace == 2 && threadIdx.x == 0) ? gtimer() : 0;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem + C::kOffQ;
   uint8_t* sDO = smem + C::kOffDO;
@@ -892,8 +910,305 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<C::kTmemCols>(tbase);
+  if (a.trace == 2 && threadIdx.x == 0 && blockIdx.x < 32768) {
+    long long* e = g_cta_tl + 4 * blockIdx.x;
+    e[0] = t_entry;
+    e[1] = gtimer();
+    e[2] = n_kt;
+    e[3] = smid();
+  }
 }
 
+
+
+// ================================================================ dQ, persistent
+// One CTA per SM walks the dQ work units (same unit order as the one-CTA-per-
+// unit grid: (sequence, kv head)-major, LPT rank, q-head) with a static
+// stride.  The TMA / MMA / compute pipelines run on across units, so the
+// per-unit prologue (TMEM alloc, barrier init, Q / dO / first K, V loads, the
+// first S and dP) and epilogue overlap the neighbouring units' work instead of
+// costing ~5 us per unit (BD_TRACE=2 timeline: 11% of the one-CTA-per-unit
+// kernel).  Q / dO of unit u+1 load as soon as the last S and dP MMAs of unit
+// u are issued; the first dQ MMA of unit u+1 waits for the compute warps to
+// have drained unit u's accumulator from TMEM.
+struct DqUnit {
+  int b, h, qt, n_kt, q0, q1, qseg;
+  const int* ents;
+  Geom g;
+  bool valid;
+};
+
+template <bool VARLEN>
+__device__ __forceinline__ DqUnit dq_unit(const BwdArgs& a, int u) {
+  const Geom& gm = a.g;
+  DqUnit r;
+  const int per_unit = gm.NT * a.group;
+  const int unit = u / per_unit;
+  const int rem = u - unit * per_unit;
+  const int rank = rem / a.group;
+  const int mi = unit / a.n_kv_heads;
+  const int kvh = unit - mi * a.n_kv_heads;
+  r.h = kvh * a.group + (rem - rank * a.group);
+  const int* mapb = VARLEN ? a.map + (size_t)mi * a.map_stride : a.map;
+  r.b = VARLEN ? map_seq(mapb) : mi;
+  r.g = VARLEN ? map_geom(mapb) : gm;
+  r.valid = !(VARLEN && rank >= r.g.NT);
+  if (!r.valid) {
+    r.n_kt = 0;
+    return r;
+  }
+  const MapView mv{const_cast<int*>(mapb), r.g.NT, map_capacity(r.g)};
+  r.qt = mv.fwd_order()[rank];
+  const int e0 = mv.row_ptr()[r.qt];
+  r.n_kt = mv.row_ptr()[r.qt + 1] - e0;
+  r.ents = mv.row_ent() + e0;
+  tile_bounds(r.g, r.qt, r.q0, r.q1, r.qseg);
+  return r;
+}
+
+template <int D, bool VARLEN>
+__global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
+    attn_bwd_dqp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                        const BwdArgs a, int n_units) {
+  using C = DqCfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sQ = smem + C::kOffQ;
+  uint8_t* sDO = smem + C::kOffDO;
+  uint8_t* sRing = smem + C::kOffRing;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + C::kStages;
+  uint64_t* s_full = kv_empty + C::kStages;  // [2]
+  uint64_t* dp_full = s_full + 2;
+  uint64_t* dp_free = dp_full + 1;
+  uint64_t* compute_done = dp_free + 1;
+  uint64_t* acc_full = compute_done + 1;
+  uint64_t* qdo_empty = acc_full + 1;  // last S, dP of a unit done: Q / dO reusable
+  uint64_t* acc_empty = qdo_empty + 1;  // compute warps drained dQ from TMEM
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+  const int warp = (int)warp_id(), lane = (int)lane_id();
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
+
+  if (warp == 0) tmem_alloc<C::kTmemCols>(tslot);
+  if (warp == C::kTmaWarp && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int s2 = 0; s2 < C::kStages; ++s2) {
+      mbar_init(&kv_full[s2], 1);
+      mbar_init(&kv_empty[s2], 1);
+    }
+    mbar_init(&s_full[0], 1);
+    mbar_init(&s_full[1], 1);
+    mbar_init(dp_full, 1);
+    mbar_init(dp_free, C::kComputeWarps);
+    mbar_init(compute_done, C::kComputeWarps);
+    mbar_init(acc_full, 1);
+    mbar_init(qdo_empty, 1);
+    mbar_init(acc_empty, C::kComputeWarps);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == C::kTmaWarp) {
+    // ================================================================ TMA
+    if (elect_one()) {
+      int jg = 0, uu = 0;  // tiles and units this CTA has issued
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const DqUnit w = dq_unit<VARLEN>(a, u);
+        if (!w.valid) continue;
+        const int kvh = w.h / a.group;
+        mbar_wait(qdo_empty, (uint32_t)((uu & 1) ^ 1));
+        mbar_expect_tx(q_full, 2 * C::kTileBytes);
+        for (int kb = 0; kb < D / 64; ++kb) {
+          tma_load_4d(sQ + kb * 16384, &tmQ, q_full, kb * 64, w.h, w.q0, w.b);
+          tma_load_4d(sDO + kb * 16384, &tmDO, q_full, kb * 64, w.h, w.q0, w.b);
+        }
+        for (int j = 0; j < w.n_kt; ++j, ++jg) {
+          const int k0 = tile_start(w.g, entry_tile(w.ents[j]));
+#pragma unroll
+          for (int kv = 0; kv < 2; ++kv) {
+            const int stage = dq_ring_slot<C>(2 * jg + kv);
+            mbar_wait(&kv_empty[stage], dq_ring_phase<C>(2 * jg + kv) ^ 1);
+            mbar_expect_tx(&kv_full[stage], C::kTileBytes);
+            uint8_t* dst = sRing + stage * C::kTileBytes;
+            for (int kb = 0; kb < D / 64; ++kb)
+              tma_load_4d(dst + kb * 16384, kv ? &tmV : &tmK, &kv_full[stage], kb * 64, kvh, k0, w.b);
+          }
+        }
+        ++uu;
+      }
+    }
+  } else if (warp == C::kMmaWarp) {
+    // ================================================================ MMA
+    if (elect_one()) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, false, true);
+      const uint32_t qaddr = smem_u32(sQ), doaddr = smem_u32(sDO);
+      auto slot = [&](int idx) { return dq_ring_slot<C>(idx); };
+      auto ph = [&](int idx) { return dq_ring_phase<C>(idx); };
+      auto ring = [&](int idx) { return smem_u32(sRing + slot(idx) * C::kTileBytes); };
+      auto issue_s = [&](int jg) {
+        const uint32_t kaddr = ring(2 * jg);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+          umma_ss(tbase + ((jg & 1) ? C::kColS1 : C::kColS0), umma_desc_sw128(qaddr + off, 16, 1024),
+                  umma_desc_sw128(kaddr + off, 16, 1024), idesc_s, k > 0);
+        }
+        umma_commit(&s_full[jg & 1]);
+      };
+      auto issue_dp = [&](int jg) {
+        const uint32_t vaddr = ring(2 * jg + 1);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+          umma_ss(tbase + C::kColDP, umma_desc_sw128(doaddr + off, 16, 1024),
+                  umma_desc_sw128(vaddr + off, 16, 1024), idesc_s, k > 0);
+        }
+        umma_commit(dp_full);
+        umma_commit(&kv_empty[slot(2 * jg + 1)]);  // V consumed
+      };
+      int jb = 0, uu = 0;  // first global tile of the unit, units done
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const DqUnit w = dq_unit<VARLEN>(a, u);
+        if (!w.valid) continue;
+        const int n = w.n_kt;
+        mbar_wait(q_full, (uint32_t)(uu & 1));
+        mbar_wait(&kv_full[slot(2 * jb)], ph(2 * jb));
+        tc_fence_after();
+        issue_s(jb);
+        mbar_wait(&kv_full[slot(2 * jb + 1)], ph(2 * jb + 1));
+        tc_fence_after();
+        issue_dp(jb);
+        if (n == 1) umma_commit(qdo_empty);  // last S and dP of the unit issued
+        if (n > 1) {
+          mbar_wait(&kv_full[slot(2 * jb + 2)], ph(2 * jb + 2));
+          tc_fence_after();
+          issue_s(jb + 1);
+        }
+        for (int j = 0; j < n; ++j) {
+          const int jg = jb + j;
+          mbar_wait(dp_free, (uint32_t)(jg & 1));
+          if (j + 1 < n) {
+            mbar_wait(&kv_full[slot(2 * jg + 3)], ph(2 * jg + 3));
+            tc_fence_after();
+            issue_dp(jg + 1);
+            if (j + 2 == n) umma_commit(qdo_empty);  // dP(n-1) follows S(n-1)
+          }
+          mbar_wait(compute_done, (uint32_t)(jg & 1));
+          if (j == 0) mbar_wait(acc_empty, (uint32_t)((uu & 1) ^ 1));  // previous unit's dQ drained
+          tc_fence_after();
+          const uint32_t sbase = tbase + ((jg & 1) ? C::kColS1 : C::kColS0);
+          const uint32_t kaddr = ring(2 * jg);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            umma_ts(tbase + C::kColDQ, sbase + 32 * (k >> 1) + 8 * (k & 1),
+                    umma_desc_sw128(kaddr + k * 2048, 16384, 1024), idesc_q, (j > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&kv_empty[slot(2 * jg)]);  // K consumed
+          if (j + 2 < n) {
+            mbar_wait(&kv_full[slot(2 * jg + 4)], ph(2 * jg + 4));
+            tc_fence_after();
+            issue_s(jg + 2);
+          }
+        }
+        umma_commit(acc_full);
+        jb += n;
+        ++uu;
+      }
+    }
+  } else {
+    // ========================================================== compute
+    const int wg = warp >> 2;
+    const int r = (warp & 3) * 32 + lane;  // query row within the tile == TMEM lane
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const float sl2 = a.scale_log2;
+    const int cb = wg * 32;
+    int jg = 0, uu = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const DqUnit w = dq_unit<VARLEN>(a, u);
+      if (!w.valid) continue;
+      const Geom& g = w.g;
+      const int row = w.q0 + r;
+      int lo0, hi0, lo1, hi1;
+      row_interval(g, w.qseg, row, 0, lo0, hi0);
+      row_interval(g, w.qseg, row, w.qseg ? w.qseg : 1, lo1, hi1);  // the row's own noisy copy
+      const size_t vslot = (((size_t)w.b * a.n_q_heads + w.h) * a.g.NT + w.qt) * kTileRows + r;
+      const float nlse2 = a.lse2_t[vslot];
+      const float ndsum = a.dsum_t[vslot];
+      int ent_next = w.ents[0];
+      for (int j = 0; j < w.n_kt; ++j, ++jg) {
+        const int ent = ent_next;
+        if (j + 1 < w.n_kt) ent_next = w.ents[j + 1];
+        const int kt = entry_tile(ent);
+        const int k0 = tile_start(g, kt), k1 = tile_end(g, kt);
+        const bool need_mask = entry_kind(ent) == kKindPartial || (k1 - k0) < 128;
+        const bool xt = tile_seg(g, kt) != 0;
+        const int lo = (xt ? lo1 : lo0) - k0;
+        const int hi = min(xt ? hi1 : hi0, k1) - k0;
+        const uint32_t sbase = tbase + lane_off + ((jg & 1) ? C::kColS1 : C::kColS0);
+        mbar_wait(&s_full[jg & 1], (uint32_t)((jg >> 1) & 1));
+        tc_fence_after();
+        float pv[32];
+        {
+          uint32_t sr[32];
+          tmem_ld32(sbase + cb, sr);
+          tmem_ld_wait();
+          if (need_mask)
+            p_row<true>(sr, nlse2, sl2, lo - cb, hi - cb, pv);
+          else
+            p_row<false>(sr, nlse2, sl2, 0, 32, pv);
+        }
+        mbar_wait(dp_full, (uint32_t)(jg & 1));
+        tc_fence_after();
+        uint32_t pk[16];
+        {
+          uint32_t dr[32];
+          tmem_ld32(tbase + lane_off + C::kColDP + cb, dr);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dp_free);
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const float2 ds = fmul2(make_float2(pv[2 * jj], pv[2 * jj + 1]),
+                                    fadd2(make_float2(__uint_as_float(dr[2 * jj]), __uint_as_float(dr[2 * jj + 1])),
+                                          make_float2(ndsum, ndsum)));
+            pk[jj] = pack_bf16x2(ds.x, ds.y);
+          }
+        }
+        tmem_st16(sbase + cb, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(compute_done);
+      }
+      // ---- epilogue of the unit: dQ = scale * acc -> bf16
+      mbar_wait(acc_full, (uint32_t)(uu & 1));
+      tc_fence_after();
+      constexpr int DC = D / C::kWGs;
+      uint32_t v[32];
+      if (DC == 32)
+        tmem_ld32(tbase + lane_off + C::kColDQ + wg * DC, v);
+      else
+        tmem_ld16(tbase + lane_off + C::kColDQ + wg * DC, v);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);  // accumulator free for the next unit
+      __nv_bfloat16* out = a.dq + (((size_t)w.b * a.N + row) * a.n_q_heads + w.h) * D + wg * DC;
+      store_row_bf16_n<DC>(out, v, a.scale, row < w.q1);
+      ++uu;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<C::kTmemCols>(tbase);
+}
 
 template <typename K>
 int set_smem(K kernel, int bytes, bool& done) {
@@ -945,8 +1260,8 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   a.g = g;
   a.scale = scale_of(p);
   a.scale_log2 = a.scale * kLog2e;
-  static const bool trace_on = getenv("BD_TRACE") != nullptr;
-  a.trace = trace_on ? 1 : 0;
+  static const int trace_on = getenv("BD_TRACE") ? atoi(getenv("BD_TRACE")) : 0;
+  a.trace = trace_on;
   // 2. dK, dV
   const long long grid_kv = (long long)g.NT * p.batch * p.n_kv_heads;
   attn_bwd_dkdv_kernel<D, VARLEN><<<(unsigned)grid_kv, DkdvCfg<D>::kThreads, DkdvCfg<D>::kSmemBytes, stream>>>(
@@ -955,6 +1270,21 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   // 3. dQ
   const long long grid_q = (long long)g.NT * p.batch * Hq;
   if (grid_q > 0x7FFFFFFF) return set_error(BD_ERR_UNSUPPORTED, "grid too large");
+  if (BD_DQ_PERSIST) {
+    static int n_sm = 0;
+    if (!n_sm) {
+      int dev = 0;
+      if ((rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice"))) return rc;
+      if ((rc = check_cuda(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev), "SM count"))) return rc;
+    }
+    static bool attr_qp = false;
+    if ((rc = set_smem(attn_bwd_dqp_kernel<D, VARLEN>, DqCfg<D>::kSmemBytes, attr_qp))) return rc;
+    const int grid_p = (int)(grid_q < n_sm ? grid_q : n_sm);
+    attn_bwd_dqp_kernel<D, VARLEN><<<(unsigned)grid_p, DqCfg<D>::kThreads, DqCfg<D>::kSmemBytes, stream>>>(
+        tmQ, tmK, tmV, tmDO, a, (int)grid_q);
+    note_launches(4);  // zero, pre, dkdv, dq
+    return check_cuda(cudaGetLastError(), "attn_bwd_dqp_kernel launch");
+  }
   attn_bwd_dq_kernel<D, VARLEN><<<(unsigned)grid_q, DqCfg<D>::kThreads, DqCfg<D>::kSmemBytes, stream>>>(tmQ, tmK, tmV,
                                                                                                tmDO, a);
   note_launches(4);  // zero, pre, dkdv, dq
@@ -982,6 +1312,10 @@ int run_attn_bwd(const bd_problem& p, const Geom& g, const void* q, const void* 
 
 }  // namespace bd
 
+extern "C" int bd_debug_cta_timeline(int64_t* host_out, int n) {
+  if (!host_out || n <= 0 || n > 4 * 32768) return BD_ERR_INVALID_ARG;
+  return bd::check_cuda(cudaMemcpyFromSymbol(host_out, bd::g_cta_tl, n * sizeof(long long)), "timeline copy");
+}
 extern "C" int bd_debug_trace(int64_t* host_out, int n) {
   if (!host_out || n <= 0 || n > 8192) return BD_ERR_INVALID_ARG;
   return bd::check_cuda(cudaMemcpyFromSymbol(host_out, bd::g_trace, n * sizeof(long long)), "trace copy");
