@@ -95,8 +95,9 @@ __global__ void zero_kernel(float4* __restrict__ p, size_t n4) {
 // stamps of its pipeline hand-offs into a static device buffer, read back by
 // bd_debug_trace().  Off by default (a warp-uniform predicate per event).
 __device__ long long g_trace[8192];
-// BD_TRACE=2: per-CTA timeline of the dQ kernel (globaltimer ns at entry and
-// exit, tile count, SM id) for the first 32768 CTAs, read by bd_debug_cta_timeline()
+// BD_TRACE=2: per-unit timeline of the dQ kernel (globaltimer ns when the
+// compute warps start the unit and after its epilogue, tile count, SM id) for
+// the first 32768 units, read by bd_debug_cta_timeline()
 __device__ long long g_cta_tl[4 * 32768];
 __device__ __forceinline__ long long gtimer() {
   long long t;
@@ -158,15 +159,6 @@ __device__ __forceinline__ void store_row_bf16_n(__nv_bfloat16* dst, const uint3
 #ifndef BD_DKDV_POLY_MOD
 #define BD_DKDV_POLY_MOD 0
 #endif
-#ifndef BD_EXP_NOVEC
-#define BD_EXP_NOVEC 0
-#endif
-#ifndef BD_DQ_PERSIST
-#define BD_DQ_PERSIST 1
-#endif
-#ifndef BD_DKDV_SPLIT
-#define BD_DKDV_SPLIT 1
-#endif
 #ifndef BD_DQ_POLY_MOD
 #define BD_DQ_POLY_MOD 0
 #endif
@@ -181,13 +173,8 @@ template <bool MASKED, int NC>
 __device__ __forceinline__ void p_tile(const uint32_t* sr, const float* sv, float sl2, int ja, int jb, float* pv) {
 #pragma unroll
   for (int j = 0; j < NC; j += 2) {  // sv = -lse2 (negated by bwd_pre)
-#if BD_EXP_NOVEC  // timing experiment only (wrong numerics): one LDS instead of 16
-    const float2 x = ffma2(make_float2(__uint_as_float(sr[j]), __uint_as_float(sr[j + 1])), make_float2(sl2, sl2),
-                           make_float2(sv[0], sv[0]));
-#else
     const float2 x = ffma2(make_float2(__uint_as_float(sr[j]), __uint_as_float(sr[j + 1])), make_float2(sl2, sl2),
                            make_float2(sv[j], sv[j + 1]));
-#endif
     const float2 p = ex2_pair<BD_DKDV_POLY_MOD>(j / 2, x);
     pv[j] = p.x;
     pv[j + 1] = p.y;
@@ -418,7 +405,6 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
           tc_fence_after();
           issue_s(i + 1);
         }
-#if BD_DKDV_SPLIT
         // P^T / dS^T arrive in two halves (q columns 0-15 and 16-31 of every
         // warpgroup = the even and odd k-steps): the even k-steps of dV(i) and
         // dK(i) run while the compute warps finish the odd half
@@ -445,22 +431,6 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
           umma_ts(tbase + C::kColDK, tbase + C::kColDP + 32 * (k >> 1) + 24,
                   umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, 1u);
         TRACE(1024 + 8 * (i & 127) + 5, blockIdx.x == 0);
-#else
-        mbar_wait(pt_done, i & 1);
-        TRACE(1024 + 8 * (i & 127) + 1, blockIdx.x == 0);
-        tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < 8; ++k)  // dV += P^T dO; P^T of q block k at dP cols 32(k/2) + 8(k%2)
-          umma_ts(tbase + C::kColDV, tbase + C::kColDP + 32 * (k >> 1) + 8 * (k & 1),
-                  umma_desc_sw128(doaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
-        umma_commit(&slot_empty[slot_of(2 * i + 1)]);  // dO(i) consumed
-        TRACE(1024 + 8 * (i & 127) + 3, blockIdx.x == 0);
-#pragma unroll
-        for (int k = 0; k < 8; ++k)  // dK += dS^T Q; dS^T (TMEM) of q block k at dP cols 32(k/2) + 16 + 8(k%2)
-          umma_ts(tbase + C::kColDK, tbase + C::kColDP + 32 * (k >> 1) + 16 + 8 * (k & 1),
-                  umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
-        TRACE(1024 + 8 * (i & 127) + 5, blockIdx.x == 0);
-#endif
         umma_commit(&slot_empty[slot_of(2 * i)]);  // Q(i) consumed
         if (has_next) {
           mbar_wait(&slot_full[slot_of(2 * i + 3)], phase_of(2 * i + 3));
@@ -526,34 +496,27 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
         }
       }
       TRACE(8 * (i & 127) + 2, blockIdx.x == 0 && threadIdx.x == 0);
-      // phase 2: dS = P (dP - D); P^T (bf16) over the dP^T columns just read
+      // phase 2: dS = P (dP - D); P^T, dS^T (bf16) over the dP^T columns just
+      // read, in two halves (q columns 0-15 and 16-31 of the warpgroup = the
+      // even and odd k-steps of dV / dK): the even k-steps of dV(i), dK(i) run
+      // while the odd half is computed
       mbar_wait(dp_full, i & 1);
       TRACE(8 * (i & 127) + 3, blockIdx.x == 0 && threadIdx.x == 0);
       tc_fence_after();
-      uint32_t dsk[NC / 2];
+      static_assert(NC == 32, "split P^T arrival assumes 32 q columns per warpgroup");
       {
-        uint32_t dr[NC];
+        uint32_t dr[NC], dsk[NC / 2], pk[NC / 2];
         tmem_ld32(tP, dr);
         tmem_ld_wait();
-        uint32_t pk[NC / 2];
-#if BD_DKDV_SPLIT
-        static_assert(NC == 32, "split P^T arrival assumes 32 q columns per warpgroup");
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
 #pragma unroll
           for (int j = 8 * hh; j < 8 * hh + 8; ++j) {
-            const float p0 = pv[2 * j], p1 = pv[2 * j + 1];
-#if BD_EXP_NOVEC
-            const float2 ds = fmul2(make_float2(p0, p1),
-                                    fadd2(make_float2(__uint_as_float(dr[2 * j]), __uint_as_float(dr[2 * j + 1])),
-                                          make_float2(sv[128], sv[128])));
-#else
-            const float2 ds = fmul2(make_float2(p0, p1),
+            const float2 ds = fmul2(make_float2(pv[2 * j], pv[2 * j + 1]),
                                     fadd2(make_float2(__uint_as_float(dr[2 * j]), __uint_as_float(dr[2 * j + 1])),
                                           make_float2(sv[128 + 2 * j], sv[128 + 2 * j + 1])));  // sv = -D
-#endif
             dsk[j] = pack_bf16x2(ds.x, ds.y);
-            pk[j] = pack_bf16x2(p0, p1);
+            pk[j] = pack_bf16x2(pv[2 * j], pv[2 * j + 1]);
           }
           tmem_st8(tP + 8 * hh, pk + 8 * hh);
           tmem_st8(tP + 16 + 8 * hh, dsk + 8 * hh);  // dS^T (bf16) beside P^T: A of dK += dS^T Q
@@ -564,19 +527,6 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
             if (lane == 0) mbar_arrive(pt_half);
           }
         }
-#else
-#pragma unroll
-        for (int j = 0; j < NC / 2; ++j) {
-          const float p0 = pv[2 * j], p1 = pv[2 * j + 1];
-          const float2 ds = fmul2(make_float2(p0, p1),
-                                  fadd2(make_float2(__uint_as_float(dr[2 * j]), __uint_as_float(dr[2 * j + 1])),
-                                        make_float2(sv[128 + 2 * j], sv[128 + 2 * j + 1])));  // sv = -D
-          dsk[j] = pack_bf16x2(ds.x, ds.y);
-          pk[j] = pack_bf16x2(p0, p1);
-        }
-        tmem_st16(tP, pk);
-        tmem_st16(tP + 16, dsk);  // dS^T (bf16) beside P^T: the A operand of dK += dS^T Q
-#endif
       }
       tmem_st_wait();
       tc_fence_before();
@@ -624,7 +574,7 @@ template <int D>
 struct DqCfg {
   static constexpr int kTileBytes = 128 * D * 2;
   // K tiles live from S(j) to dQ(j), V tiles only until dP(j): separate rings,
-  // K(j) -> slot j % 3, V(j) -> slot 3 + j % 2 (ring index 2j / 2j+1).
+  // K(j) -> slot j % kKSlots, V(j) -> slot kKSlots + j % kVSlots (ring index 2j / 2j+1).
 #ifndef BD_DQ_KSLOTS
 #define BD_DQ_KSLOTS 4
 #endif
@@ -643,9 +593,9 @@ struct DqCfg {
   static constexpr int kOffDO = kTileBytes;
   static constexpr int kOffRing = 2 * kTileBytes;
   static constexpr int kOffBar = kOffRing + kStages * kTileBytes;
-  // q_full, kv_full[S], kv_empty[S], s_full[2], dp_full, dp_free, compute_done, acc_done
-  // (+ qdo_empty, acc_empty in the persistent kernel)
-  static constexpr int kNumBars = 1 + 2 * kStages + 8;
+  // q_full, kv_full[S], kv_empty[S], s_full[2], dp_full, dp_free, compute_done[2], acc_full,
+  // qdo_empty, acc_empty
+  static constexpr int kNumBars = 1 + 2 * kStages + 9;
   static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16;
 };
 
@@ -660,266 +610,6 @@ __device__ __forceinline__ uint32_t dq_ring_phase(int idx) {
   const int j = idx >> 1;
   return (uint32_t)(((idx & 1) ? j / C::kVSlots : j / C::kKSlots) & 1);
 }
-
-template <int D, bool VARLEN>
-__global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
-    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                       const BwdArgs a) {
-  using C = DqCfg<D>;
-  const long long t_entry = (a.trace == 2 && threadIdx.x == 0) ? gtimer() : 0;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sQ = smem + C::kOffQ;
-  uint8_t* sDO = smem + C::kOffDO;
-  uint8_t* sRing = smem + C::kOffRing;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
-  uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = kv_full + C::kStages;
-  uint64_t* s_full = kv_empty + C::kStages;  // [2]
-  uint64_t* dp_full = s_full + 2;
-  uint64_t* dp_free = dp_full + 1;       // compute has read dP(j)
-  uint64_t* compute_done = dp_free + 1;  // dS(j) written over S[j&1]
-  uint64_t* acc_done = compute_done + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
-
-  const int warp = (int)warp_id(), lane = (int)lane_id();
-  const Geom& gm = a.g;  // the batch's (maximum) geometry: grid, vector strides
-  if ((smem_u32(smem) & 1023u) != 0) __trap();
-
-  // Grid order: (sequence, kv head) outermost, then the q-tile's LPT rank,
-  // then the q-heads of the group (they share every K/V tile: L2 reuse).
-  const int per_unit = gm.NT * a.group;
-  const int unit = blockIdx.x / per_unit;
-  const int rem = blockIdx.x - unit * per_unit;
-  const int rank = rem / a.group;
-  const int mi = unit / a.n_kv_heads;  // map slot (varlen: longest sequences first)
-  const int kvh = unit - mi * a.n_kv_heads;
-  const int h = kvh * a.group + (rem - rank * a.group);
-  const int* mapb = VARLEN ? a.map + (size_t)mi * a.map_stride : a.map;
-  const int b = VARLEN ? map_seq(mapb) : mi;
-  const Geom gsq = VARLEN ? map_geom(mapb) : gm;
-  const Geom& g = VARLEN ? gsq : gm;
-  if (VARLEN && rank >= g.NT) return;
-  const MapView mv{const_cast<int*>(mapb), g.NT, map_capacity(g)};
-  const int qt = mv.fwd_order()[rank];
-  const int e0 = mv.row_ptr()[qt];
-  const int n_kt = mv.row_ptr()[qt + 1] - e0;
-  const int* ents = mv.row_ent() + e0;
-  int q0, q1, qseg;
-  tile_bounds(g, qt, q0, q1, qseg);
-
-  if (warp == 0) tmem_alloc<C::kTmemCols>(tslot);
-  if (warp == C::kTmaWarp && lane == 0) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
-    }
-    mbar_init(&s_full[0], 1);
-    mbar_init(&s_full[1], 1);
-    mbar_init(dp_full, 1);
-    mbar_init(dp_free, C::kComputeWarps);
-    mbar_init(compute_done, C::kComputeWarps);
-    mbar_init(acc_done, 1);
-    fence_barrier_init();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = *tslot;
-
-  if (warp == C::kTmaWarp) {
-    // ================================================================ TMA
-    if (elect_one()) {
-      mbar_expect_tx(q_full, 2 * C::kTileBytes);
-      for (int kb = 0; kb < D / 64; ++kb) {
-        tma_load_4d(sQ + kb * 16384, &tmQ, q_full, kb * 64, h, q0, b);
-        tma_load_4d(sDO + kb * 16384, &tmDO, q_full, kb * 64, h, q0, b);
-      }
-      for (int j = 0; j < n_kt; ++j) {
-        const int k0 = tile_start(g, entry_tile(ents[j]));
-#pragma unroll
-        for (int kv = 0; kv < 2; ++kv) {
-          const int stage = dq_ring_slot<C>(2 * j + kv);
-          mbar_wait(&kv_empty[stage], dq_ring_phase<C>(2 * j + kv) ^ 1);
-          mbar_expect_tx(&kv_full[stage], C::kTileBytes);
-          uint8_t* dst = sRing + stage * C::kTileBytes;
-          for (int kb = 0; kb < D / 64; ++kb)
-            tma_load_4d(dst + kb * 16384, kv ? &tmV : &tmK, &kv_full[stage], kb * 64, kvh, k0, b);
-        }
-      }
-    }
-  } else if (warp == C::kMmaWarp) {
-    // ================================================================ MMA
-    if (elect_one()) {
-      constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);  // S = Q K^T, dP = dO V^T
-      constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, false, true);     // dQ += dS K (B MN-major)
-      const uint32_t qaddr = smem_u32(sQ), doaddr = smem_u32(sDO);
-      auto slot = [&](int idx) { return dq_ring_slot<C>(idx); };
-      auto ph = [&](int idx) { return dq_ring_phase<C>(idx); };
-      auto ring = [&](int idx) { return smem_u32(sRing + slot(idx) * C::kTileBytes); };
-      auto issue_s = [&](int j) {
-        const uint32_t kaddr = ring(2 * j);
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
-          umma_ss(tbase + ((j & 1) ? C::kColS1 : C::kColS0), umma_desc_sw128(qaddr + off, 16, 1024),
-                  umma_desc_sw128(kaddr + off, 16, 1024), idesc_s, k > 0);
-        }
-        umma_commit(&s_full[j & 1]);
-      };
-      auto issue_dp = [&](int j) {
-        const uint32_t vaddr = ring(2 * j + 1);
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
-          umma_ss(tbase + C::kColDP, umma_desc_sw128(doaddr + off, 16, 1024),
-                  umma_desc_sw128(vaddr + off, 16, 1024), idesc_s, k > 0);
-        }
-        umma_commit(dp_full);
-        umma_commit(&kv_empty[slot(2 * j + 1)]);  // V(j) consumed
-      };
-      // Prologue S(0), dP(0), S(1); then per tile, after compute(j): dQ(j),
-      // dP(j+1) (dP region read by compute(j)), S(j+2) into the buffer dQ(j)
-      // has just consumed.  compute(j+1) phase 1 (exp of S(j+1)) overlaps
-      // dQ(j) and dP(j+1).
-      mbar_wait(q_full, 0);
-      mbar_wait(&kv_full[slot(0)], ph(0));
-      tc_fence_after();
-      issue_s(0);
-      mbar_wait(&kv_full[slot(1)], ph(1));
-      tc_fence_after();
-      issue_dp(0);
-      if (n_kt > 1) {
-        mbar_wait(&kv_full[slot(2)], ph(2));
-        tc_fence_after();
-        issue_s(1);
-      }
-      for (int j = 0; j < n_kt; ++j) {
-        mbar_wait(dp_free, j & 1);
-        TRACE(5120 + 8 * (j & 127) + 0, blockIdx.x == 0);
-        if (j + 1 < n_kt) {
-          mbar_wait(&kv_full[slot(2 * j + 3)], ph(2 * j + 3));
-          tc_fence_after();
-          issue_dp(j + 1);
-        }
-        mbar_wait(compute_done, j & 1);
-        TRACE(5120 + 8 * (j & 127) + 1, blockIdx.x == 0);
-        tc_fence_after();
-        // dQ += dS(j) K(j): A = dS bf16 in S[j&1]; keys 32w..32w+31 at cols 32w..32w+15
-        const uint32_t sbase = tbase + ((j & 1) ? C::kColS1 : C::kColS0);
-        const uint32_t kaddr = ring(2 * j);
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          umma_ts(tbase + C::kColDQ, sbase + 32 * (k >> 1) + 8 * (k & 1),
-                  umma_desc_sw128(kaddr + k * 2048, 16384, 1024), idesc_q, (j > 0 || k > 0) ? 1u : 0u);
-        umma_commit(&kv_empty[slot(2 * j)]);  // K(j) consumed
-        if (j + 2 < n_kt) {
-          mbar_wait(&kv_full[slot(2 * j + 4)], ph(2 * j + 4));
-          // dQ(j) reads dS(j) from S[j&1]; S(j+2) may follow it at once (in-order tensor pipe)
-          TRACE(5120 + 8 * (j & 127) + 2, blockIdx.x == 0);
-          tc_fence_after();
-          issue_s(j + 2);
-        }
-      }
-      umma_commit(acc_done);
-    }
-  } else {
-    // ========================================================== compute
-    const int wg = warp >> 2;
-    const int r = (warp & 3) * 32 + lane;  // query row within the tile == TMEM lane
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const float sl2 = a.scale_log2;
-    const int row = q0 + r;
-    int lo0, hi0, lo1, hi1;
-    row_interval(g, qseg, row, 0, lo0, hi0);
-    row_interval(g, qseg, row, qseg ? qseg : 1, lo1, hi1);  // the row's own noisy copy
-    const size_t vslot = (((size_t)b * a.n_q_heads + h) * gm.NT + qt) * kTileRows + r;
-    const float nlse2 = a.lse2_t[vslot];  // -lse2 and -D (negated by bwd_pre)
-    const float ndsum = a.dsum_t[vslot];
-    int ent_next = n_kt > 0 ? ents[0] : 0;  // row entries loaded one tile ahead
-    for (int j = 0; j < n_kt; ++j) {
-      const int ent = ent_next;
-      if (j + 1 < n_kt) ent_next = ents[j + 1];
-      const int kt = entry_tile(ent);
-      const int k0 = tile_start(g, kt), k1 = tile_end(g, kt);
-      const bool need_mask = entry_kind(ent) == kKindPartial || (k1 - k0) < 128;
-      const bool xt = tile_seg(g, kt) != 0;
-      const int lo = (xt ? lo1 : lo0) - k0;
-      const int hi = min(xt ? hi1 : hi0, k1) - k0;
-      const uint32_t sbase = tbase + lane_off + ((j & 1) ? C::kColS1 : C::kColS0);
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
-      TRACE(4096 + 8 * (j & 127) + 0, blockIdx.x == 0 && threadIdx.x == 0);
-      tc_fence_after();
-      // phase 1: P = exp2(S sl2 - lse2) for this warpgroup's 32 key columns
-      const int cb = wg * 32;
-      float pv[32];
-      {
-        uint32_t sr[32];
-        tmem_ld32(sbase + cb, sr);
-        tmem_ld_wait();
-        if (need_mask)
-          p_row<true>(sr, nlse2, sl2, lo - cb, hi - cb, pv);
-        else
-          p_row<false>(sr, nlse2, sl2, 0, 32, pv);
-      }
-      // phase 2: dS = P (dP - D) -> bf16 over the S columns already read
-      mbar_wait(dp_full, j & 1);
-      TRACE(4096 + 8 * (j & 127) + 1, blockIdx.x == 0 && threadIdx.x == 0);
-      tc_fence_after();
-      uint32_t pk[16];
-      {
-        uint32_t dr[32];
-        tmem_ld32(tbase + lane_off + C::kColDP + cb, dr);
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(dp_free);  // dP(j) read: dP(j+1) may be issued
-        TRACE(4096 + 8 * (j & 127) + 2, blockIdx.x == 0 && threadIdx.x == 0);
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj)
-        {
-          const float2 ds = fmul2(make_float2(pv[2 * jj], pv[2 * jj + 1]),
-                                  fadd2(make_float2(__uint_as_float(dr[2 * jj]), __uint_as_float(dr[2 * jj + 1])),
-                                        make_float2(ndsum, ndsum)));
-          pk[jj] = pack_bf16x2(ds.x, ds.y);
-        }
-      }
-      tmem_st16(sbase + cb, pk);
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(compute_done);
-      TRACE(4096 + 8 * (j & 127) + 3, blockIdx.x == 0 && threadIdx.x == 0);
-    }
-    // ---- epilogue: dQ = scale * acc -> bf16
-    mbar_wait(acc_done, 0);
-    tc_fence_after();
-    const bool ok = row < q1;
-    constexpr int DC = D / C::kWGs;
-    __nv_bfloat16* out = a.dq + (((size_t)b * a.N + row) * a.n_q_heads + h) * D + wg * DC;
-    uint32_t v[32];
-    if (DC == 32)
-      tmem_ld32(tbase + lane_off + C::kColDQ + wg * DC, v);
-    else
-      tmem_ld16(tbase + lane_off + C::kColDQ + wg * DC, v);
-    tmem_ld_wait();
-    store_row_bf16_n<DC>(out, v, a.scale, ok);
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc<C::kTmemCols>(tbase);
-  if (a.trace == 2 && threadIdx.x == 0 && blockIdx.x < 32768) {
-    long long* e = g_cta_tl + 4 * blockIdx.x;
-    e[0] = t_entry;
-    e[1] = gtimer();
-    e[2] = n_kt;
-    e[3] = smid();
-  }
-}
-
-
 
 // ================================================================ dQ, persistent
 // One CTA per SM walks the dQ work units (same unit order as the one-CTA-per-
@@ -983,8 +673,11 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
   uint64_t* s_full = kv_empty + C::kStages;  // [2]
   uint64_t* dp_full = s_full + 2;
   uint64_t* dp_free = dp_full + 1;
+  // [2]: dS(jg) written, one barrier per S buffer -- the warps can reach tile
+  // jg+1 (its dP was issued before the MMA thread waits for tile jg), never
+  // jg+2 (its S is issued after that wait), so no phase passes unobserved
   uint64_t* compute_done = dp_free + 1;
-  uint64_t* acc_full = compute_done + 1;
+  uint64_t* acc_full = compute_done + 2;
   uint64_t* qdo_empty = acc_full + 1;  // last S, dP of a unit done: Q / dO reusable
   uint64_t* acc_empty = qdo_empty + 1;  // compute warps drained dQ from TMEM
   uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 1);
@@ -1003,7 +696,8 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
     mbar_init(&s_full[1], 1);
     mbar_init(dp_full, 1);
     mbar_init(dp_free, C::kComputeWarps);
-    mbar_init(compute_done, C::kComputeWarps);
+    mbar_init(&compute_done[0], C::kComputeWarps);
+    mbar_init(&compute_done[1], C::kComputeWarps);
     mbar_init(acc_full, 1);
     mbar_init(qdo_empty, 1);
     mbar_init(acc_empty, C::kComputeWarps);
@@ -1042,6 +736,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         }
         ++uu;
       }
+      if (uu > 0) mbar_wait(qdo_empty, (uint32_t)((uu - 1) & 1));  // observe the last unit's release
     }
   } else if (warp == C::kMmaWarp) {
     // ================================================================ MMA
@@ -1100,7 +795,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
             issue_dp(jg + 1);
             if (j + 2 == n) umma_commit(qdo_empty);  // dP(n-1) follows S(n-1)
           }
-          mbar_wait(compute_done, (uint32_t)(jg & 1));
+          mbar_wait(&compute_done[jg & 1], (uint32_t)((jg >> 1) & 1));
           if (j == 0) mbar_wait(acc_empty, (uint32_t)((uu & 1) ^ 1));  // previous unit's dQ drained
           tc_fence_after();
           const uint32_t sbase = tbase + ((jg & 1) ? C::kColS1 : C::kColS0);
@@ -1120,6 +815,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         jb += n;
         ++uu;
       }
+      if (uu > 0) mbar_wait(acc_empty, (uint32_t)((uu - 1) & 1));  // observe the last drain
     }
   } else {
     // ========================================================== compute
@@ -1132,6 +828,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const DqUnit w = dq_unit<VARLEN>(a, u);
       if (!w.valid) continue;
+      const long long t_unit = (a.trace == 2 && threadIdx.x == 0) ? gtimer() : 0;
       const Geom& g = w.g;
       const int row = w.q0 + r;
       int lo0, hi0, lo1, hi1;
@@ -1185,7 +882,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(compute_done);
+        if (lane == 0) mbar_arrive(&compute_done[jg & 1]);
       }
       // ---- epilogue of the unit: dQ = scale * acc -> bf16
       mbar_wait(acc_full, (uint32_t)(uu & 1));
@@ -1202,6 +899,13 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
       if (lane == 0) mbar_arrive(acc_empty);  // accumulator free for the next unit
       __nv_bfloat16* out = a.dq + (((size_t)w.b * a.N + row) * a.n_q_heads + w.h) * D + wg * DC;
       store_row_bf16_n<DC>(out, v, a.scale, row < w.q1);
+      if (a.trace == 2 && threadIdx.x == 0 && u < 32768) {
+        long long* e = g_cta_tl + 4 * u;
+        e[0] = t_unit;
+        e[1] = gtimer();
+        e[2] = w.n_kt;
+        e[3] = smid();
+      }
       ++uu;
     }
   }
@@ -1243,7 +947,7 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   static bool attr_kv = false, attr_q = false;
   int rc = set_smem(attn_bwd_dkdv_kernel<D, VARLEN>, DkdvCfg<D>::kSmemBytes, attr_kv);
   if (rc) return rc;
-  if ((rc = set_smem(attn_bwd_dq_kernel<D, VARLEN>, DqCfg<D>::kSmemBytes, attr_q))) return rc;
+  if ((rc = set_smem(attn_bwd_dqp_kernel<D, VARLEN>, DqCfg<D>::kSmemBytes, attr_q))) return rc;
   BwdArgs a;
   a.map = map;
   a.map_stride = map_stride;
@@ -1270,25 +974,17 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   // 3. dQ
   const long long grid_q = (long long)g.NT * p.batch * Hq;
   if (grid_q > 0x7FFFFFFF) return set_error(BD_ERR_UNSUPPORTED, "grid too large");
-  if (BD_DQ_PERSIST) {
-    static int n_sm = 0;
-    if (!n_sm) {
-      int dev = 0;
-      if ((rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice"))) return rc;
-      if ((rc = check_cuda(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev), "SM count"))) return rc;
-    }
-    static bool attr_qp = false;
-    if ((rc = set_smem(attn_bwd_dqp_kernel<D, VARLEN>, DqCfg<D>::kSmemBytes, attr_qp))) return rc;
-    const int grid_p = (int)(grid_q < n_sm ? grid_q : n_sm);
-    attn_bwd_dqp_kernel<D, VARLEN><<<(unsigned)grid_p, DqCfg<D>::kThreads, DqCfg<D>::kSmemBytes, stream>>>(
-        tmQ, tmK, tmV, tmDO, a, (int)grid_q);
-    note_launches(4);  // zero, pre, dkdv, dq
-    return check_cuda(cudaGetLastError(), "attn_bwd_dqp_kernel launch");
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    if ((rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice"))) return rc;
+    if ((rc = check_cuda(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev), "SM count"))) return rc;
   }
-  attn_bwd_dq_kernel<D, VARLEN><<<(unsigned)grid_q, DqCfg<D>::kThreads, DqCfg<D>::kSmemBytes, stream>>>(tmQ, tmK, tmV,
-                                                                                               tmDO, a);
+  const int grid_p = (int)(grid_q < n_sm ? grid_q : n_sm);
+  attn_bwd_dqp_kernel<D, VARLEN><<<(unsigned)grid_p, DqCfg<D>::kThreads, DqCfg<D>::kSmemBytes, stream>>>(
+      tmQ, tmK, tmV, tmDO, a, (int)grid_q);
   note_launches(4);  // zero, pre, dkdv, dq
-  return check_cuda(cudaGetLastError(), "attn_bwd_dq_kernel launch");
+  return check_cuda(cudaGetLastError(), "attn_bwd_dqp_kernel launch");
 }
 
 }  // namespace

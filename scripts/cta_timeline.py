@@ -1,6 +1,8 @@
-"""Per-CTA timeline of the dQ kernel (run with BD_TRACE=2): how much of the
-kernel's span the SMs spend inside CTAs, and per-CTA cost vs tile count
-(fixed overhead + per-tile time, least squares).  Dev diagnostic."""
+"""Per-unit timeline of the (persistent) dQ kernel (run with BD_TRACE=2): how
+much of the kernel's span the SMs' compute warps spend inside work units, and
+per-unit cost vs tile count (fixed overhead + per-tile time, least squares).
+Dev diagnostic.  (The one-CTA-per-unit kernel it was first written for gave
+98.3% busy, ~5.3 us + 1.13 us per tile at SDAR-8B batch 2.)"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -24,7 +26,7 @@ t = np.array(buf, dtype=np.int64).reshape(n, 4)
 t0, t1, nk, sm = t[:, 0], t[:, 1], t[:, 2], t[:, 3]
 span = t1.max() - t0.min()
 dur = t1 - t0
-print(f"CTAs {n}, span {span / 1e3:.1f} us, mean CTA {dur.mean() / 1e3:.2f} us, tiles/CTA {nk.mean():.1f}")
+print(f"units {n}, span {span / 1e3:.1f} us, mean unit {dur.mean() / 1e3:.2f} us, tiles/unit {nk.mean():.1f}")
 busy = np.zeros(sm.max() + 1)
 np.add.at(busy, sm, dur)
 print(f"SM busy fraction of span: mean {busy.mean() / span:.3f} min {busy.min() / span:.3f}")
@@ -39,7 +41,7 @@ for s_ in np.unique(sm):
     a0, a1 = t0[idx][o_], t1[idx][o_]
     gaps += list(a0[1:] - a1[:-1])
 gaps = np.array(gaps)
-print(f"gap between CTAs on an SM: median {np.median(gaps) / 1e3:.2f} us, mean {gaps.mean() / 1e3:.2f} us")
+print(f"gap between units on an SM: median {np.median(gaps) / 1e3:.2f} us, mean {gaps.mean() / 1e3:.2f} us")
 for lo, hi in [(1, 5), (5, 20), (20, 40), (40, 80)]:
     m = (nk >= lo) & (nk < hi)
     if m.any():
