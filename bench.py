@@ -322,7 +322,7 @@ def run_ours(args):
     fwd_achieved = fwd_f / (phase["attn_fwd"] * 1e-3) / 1e12
     lp_bytes = step.n_rows * step.V * 2
     traffic = load_traffic() if cfg.name == "sdar_8b" else {}  # the ncu capture is at the SDAR-8B bench shape
-    roofline = {"kernel": "bd_attn_bwd (attn_bwd_dkdv_kernel + attn_bwd_dq_kernel + bwd_pre + tile map)",
+    roofline = {"kernel": "bd_attn_bwd (attn_bwd_dkdv_kernel + attn_bwd_dqp_kernel (persistent dQ) + bwd_pre + tile map)",
                 "bound": "tensor",
                 "achieved": round(bwd_achieved, 1), "peak": peak_s, "unit": "TFLOP/s",
                 "frac": round(bwd_achieved / peak_s, 4), "traffic": traffic.get("attn_bwd"),
