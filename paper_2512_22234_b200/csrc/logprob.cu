@@ -220,6 +220,9 @@ __global__ void __launch_bounds__(kThreads) logprob_bwd_kernel(int64_t n_rows, i
 // one HBM write of the logits (the two-kernel path reads them twice).
 // Requires V % (8 kCl) == 0 and 16-byte aligned rows (Qwen3 V = 151,936 is).
 constexpr int kCl = 4;
+#ifndef BD_LP_ONEBAR
+#define BD_LP_ONEBAR 1
+#endif
 #ifndef BD_LP_PACKED
 #define BD_LP_PACKED 1
 #endif
@@ -239,6 +242,12 @@ __device__ __forceinline__ float ld_dsmem_f32(const float* local, uint32_t rank)
   float v;
   asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
   return v;
+}
+
+__device__ __forceinline__ void st_dsmem_f32(float* local, uint32_t rank, float v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
 }
 
 __device__ __forceinline__ float block_reduce(float v, float* sh, bool is_max) {
@@ -266,6 +275,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float red[kFusedThreads / 32];
   __shared__ float part[2];  // [0] max, [1] sum of this CTA's slice
+  __shared__ float pall[2 * kCl];  // one-barrier mode: (max, sum) of every slice, pushed by its CTA
   __shared__ float zt;       // target logit (if in this slice)
   __shared__ __align__(8) uint64_t bar;
   const int64_t row = blockIdx.x / kCl;
@@ -279,6 +289,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
     fence_barrier_init();
   }
   __syncthreads();
+#if BD_LP_ONEBAR
+  // every CTA of the cluster must have started before a peer writes into its
+  // shared memory: arrive now, wait just before the push (overlapped with the
+  // slice load and the first two passes)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+#endif
   if (tid == 0) {
     const uint32_t bytes = (uint32_t)Vc * 2;
     mbar_expect_tx(&bar, bytes);
@@ -315,11 +331,18 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
   }
 #endif
   mx = block_reduce(mx, red, true);
+#if BD_LP_ONEBAR
+  // e is taken against the slice's own max; the slices' (max, sum) pairs are
+  // combined after a single cluster barrier
+  const float m = mx;
+  const float m2 = m == -INFINITY ? 0.f : m * kLog2e;
+#else
   if (tid == 0) part[0] = mx;
   cluster_sync_all();
   float m = -INFINITY;
   for (uint32_t r = 0; r < (uint32_t)kCl; ++r) m = fmaxf(m, ld_dsmem_f32(&part[0], r));
   const float m2 = m * kLog2e;
+#endif
   // pass 2: e = 2^(x log2e - m2) stored over the slice (bf16), partial sum
   float sum = 0.f;
 #if BD_LP_PACKED
@@ -357,11 +380,33 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
   }
 #endif
   sum = block_reduce(sum, red, false);
+#if BD_LP_ONEBAR
+  // push (max, sum) into slot `crank` of every CTA of the cluster, then one
+  // barrier; afterwards only local shared memory is read, so no trailing
+  // barrier is needed before a CTA exits
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  if (tid < kCl) {
+    st_dsmem_f32(&pall[2 * crank], (uint32_t)tid, m);
+    st_dsmem_f32(&pall[2 * crank + 1], (uint32_t)tid, sum);
+  }
+  cluster_sync_all();
+  float mg = -INFINITY;
+#pragma unroll
+  for (int r = 0; r < kCl; ++r) mg = fmaxf(mg, pall[2 * r]);
+  float tot = 0.f;
+#pragma unroll
+  for (int r = 0; r < kCl; ++r)
+    tot += pall[2 * r] == -INFINITY ? 0.f : pall[2 * r + 1] * ex2_approx((pall[2 * r] - mg) * kLog2e);
+  const float lse = mg + __logf(tot);
+  const float own = m == -INFINITY ? 0.f : ex2_approx((m - mg) * kLog2e);  // e_slice -> e_row factor
+#else
   if (tid == 0) part[1] = sum;
   cluster_sync_all();
   float tot = 0.f;
   for (uint32_t r = 0; r < (uint32_t)kCl; ++r) tot += ld_dsmem_f32(&part[1], r);
   const float lse = m + __logf(tot);
+  const float own = 1.f;
+#endif
   if (tid == 0) {
     if (crank == 0) {
       if (lse_out) lse_out[row] = lse;
@@ -369,11 +414,13 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
     }
     if (tl >= 0 && tl < Vc) logp[row] = zt - lse;
   }
+#if !BD_LP_ONEBAR
   cluster_sync_all();  // peers' DSMEM reads of `part` complete before any CTA exits
+#endif
   if (!dlogp) return;
   // pass 3: dz = w (1[v = t] - e / sum)
   const float wgt = dlogp[row];
-  const float scl = wgt / tot;
+  const float scl = wgt * own / tot;
   uint4* out = reinterpret_cast<uint4*>(dz + row * dz_stride + (int64_t)crank * Vc);
 #if BD_LP_PACKED
   {
