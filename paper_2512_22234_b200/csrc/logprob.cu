@@ -220,12 +220,6 @@ __global__ void __launch_bounds__(kThreads) logprob_bwd_kernel(int64_t n_rows, i
 // one HBM write of the logits (the two-kernel path reads them twice).
 // Requires V % (8 kCl) == 0 and 16-byte aligned rows (Qwen3 V = 151,936 is).
 constexpr int kCl = 4;
-#ifndef BD_LP_ONEBAR
-#define BD_LP_ONEBAR 1
-#endif
-#ifndef BD_LP_PACKED
-#define BD_LP_PACKED 1
-#endif
 constexpr int kFusedThreads = 256;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -235,13 +229,6 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ float ld_dsmem_f32(const float* local, uint32_t rank) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
-  return v;
 }
 
 __device__ __forceinline__ void st_dsmem_f32(float* local, uint32_t rank, float v) {
@@ -265,16 +252,17 @@ __device__ __forceinline__ float block_reduce(float v, float* sh, bool is_max) {
   return v;
 }
 
-// One exp2 per element: pass 1 row max (cluster-reduced over DSMEM), pass 2
-// e = 2^(x log2e - m) written back over the slice as bf16 plus the sum
-// (cluster-reduced), pass 3 dz = w (1[v = t] - e 2^(m - lse2)) from smem.
+// One exp2 per element and one cluster barrier per row: pass 1 the slice's
+// max, pass 2 e = 2^(x log2e - m_slice)
+// written back over the slice as bf16 plus the slice sum, the (max, sum) pairs
+// pushed to every CTA of the cluster and combined after one barrier into the
+// row's LSE, pass 3 dz = w (1[v = t] - e 2^(m_slice - M) / sum) from smem.
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
     logprob_fused_kernel(int V, const __nv_bfloat16* z, int64_t stride, const int32_t* __restrict__ targets,
                          float* __restrict__ logp, float* __restrict__ lse_out, const float* __restrict__ dlogp,
                          __nv_bfloat16* dz, int64_t dz_stride) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float red[kFusedThreads / 32];
-  __shared__ float part[2];  // [0] max, [1] sum of this CTA's slice
   __shared__ float pall[2 * kCl];  // one-barrier mode: (max, sum) of every slice, pushed by its CTA
   __shared__ float zt;       // target logit (if in this slice)
   __shared__ __align__(8) uint64_t bar;
@@ -289,12 +277,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
     fence_barrier_init();
   }
   __syncthreads();
-#if BD_LP_ONEBAR
   // every CTA of the cluster must have started before a peer writes into its
   // shared memory: arrive now, wait just before the push (overlapped with the
   // slice load and the first two passes)
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-#endif
   if (tid == 0) {
     const uint32_t bytes = (uint32_t)Vc * 2;
     mbar_expect_tx(&bar, bytes);
@@ -306,11 +292,11 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
   const int t = targets[row];
   const int tl = t - (int)crank * Vc;  // target within this slice (may fall outside)
   mbar_wait(&bar, 0);
-  if (tid == 0 && tl >= 0 && tl < Vc) zt = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(smem)[tl]);
+  // (one barrier for the whole slice: per-32 KB-piece barriers letting pass 1
+  // start on the first piece measured 1% slower)
   // pass 1: max of the slice
   const int nv = Vc / 8;
   float mx = -INFINITY;
-#if BD_LP_PACKED
   {  // packed bf16x2 max (exact): one HMNMX2 per two elements, no unpacking
     __nv_bfloat162 m2v = __float2bfloat162_rn(-INFINITY);
     for (int i = tid; i < nv; i += kFusedThreads) {
@@ -321,31 +307,14 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
     }
     mx = fmaxf(__low2float(m2v), __high2float(m2v));
   }
-#else
-  for (int i = tid; i < nv; i += kFusedThreads) {
-    const uint4 u = buf4[i];
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      mx = fmaxf(mx, fmaxf(__uint_as_float(w[j] << 16), __uint_as_float(w[j] & 0xFFFF0000u)));
-  }
-#endif
+  if (tid == 0 && tl >= 0 && tl < Vc) zt = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(smem)[tl]);
   mx = block_reduce(mx, red, true);
-#if BD_LP_ONEBAR
   // e is taken against the slice's own max; the slices' (max, sum) pairs are
   // combined after a single cluster barrier
   const float m = mx;
   const float m2 = m == -INFINITY ? 0.f : m * kLog2e;
-#else
-  if (tid == 0) part[0] = mx;
-  cluster_sync_all();
-  float m = -INFINITY;
-  for (uint32_t r = 0; r < (uint32_t)kCl; ++r) m = fmaxf(m, ld_dsmem_f32(&part[0], r));
-  const float m2 = m * kLog2e;
-#endif
   // pass 2: e = 2^(x log2e - m2) stored over the slice (bf16), partial sum
   float sum = 0.f;
-#if BD_LP_PACKED
   {  // packed fp32x2 argument (FFMA2) and sum (FADD2)
     const float2 l2e = make_float2(kLog2e, kLog2e), nm2 = make_float2(-m2, -m2);
     float2 acc = make_float2(0.f, 0.f);
@@ -364,23 +333,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
     }
     sum = acc.x + acc.y;
   }
-#else
-  for (int i = tid; i < nv; i += kFusedThreads) {
-    const uint4 u = buf4[i];
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-    uint32_t o[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float e0 = ex2_approx(fmaf(__uint_as_float(w[j] << 16), kLog2e, -m2));
-      const float e1 = ex2_approx(fmaf(__uint_as_float(w[j] & 0xFFFF0000u), kLog2e, -m2));
-      sum += e0 + e1;
-      o[j] = pack_bf16x2(e0, e1);
-    }
-    buf4[i] = make_uint4(o[0], o[1], o[2], o[3]);
-  }
-#endif
   sum = block_reduce(sum, red, false);
-#if BD_LP_ONEBAR
   // push (max, sum) into slot `crank` of every CTA of the cluster, then one
   // barrier; afterwards only local shared memory is read, so no trailing
   // barrier is needed before a CTA exits
@@ -399,14 +352,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
     tot += pall[2 * r] == -INFINITY ? 0.f : pall[2 * r + 1] * ex2_approx((pall[2 * r] - mg) * kLog2e);
   const float lse = mg + __logf(tot);
   const float own = m == -INFINITY ? 0.f : ex2_approx((m - mg) * kLog2e);  // e_slice -> e_row factor
-#else
-  if (tid == 0) part[1] = sum;
-  cluster_sync_all();
-  float tot = 0.f;
-  for (uint32_t r = 0; r < (uint32_t)kCl; ++r) tot += ld_dsmem_f32(&part[1], r);
-  const float lse = m + __logf(tot);
-  const float own = 1.f;
-#endif
   if (tid == 0) {
     if (crank == 0) {
       if (lse_out) lse_out[row] = lse;
@@ -414,15 +359,11 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
     }
     if (tl >= 0 && tl < Vc) logp[row] = zt - lse;
   }
-#if !BD_LP_ONEBAR
-  cluster_sync_all();  // peers' DSMEM reads of `part` complete before any CTA exits
-#endif
   if (!dlogp) return;
   // pass 3: dz = w (1[v = t] - e / sum)
   const float wgt = dlogp[row];
   const float scl = wgt * own / tot;
   uint4* out = reinterpret_cast<uint4*>(dz + row * dz_stride + (int64_t)crank * Vc);
-#if BD_LP_PACKED
   {
     // -scl e in packed bf16x2 arithmetic: -scl = hi + lo (two bf16), dz =
     // fma(e, hi, e lo) rounds once, to within 2^-17 of bf16(-scl e); the one
@@ -454,21 +395,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
       out[i] = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
-#else
-  for (int i = tid; i < nv; i += kFusedThreads) {
-    const uint4 u = buf4[i];
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-    uint32_t o[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int v0 = 8 * i + 2 * j;
-      const float g0 = (v0 == tl ? wgt : 0.f) - scl * __uint_as_float(w[j] << 16);
-      const float g1 = (v0 + 1 == tl ? wgt : 0.f) - scl * __uint_as_float(w[j] & 0xFFFF0000u);
-      o[j] = pack_bf16x2(g0, g1);
-    }
-    out[i] = make_uint4(o[0], o[1], o[2], o[3]);
-  }
-#endif
 }
 
 }  // namespace
