@@ -5,27 +5,30 @@
 //   dS = P o (dP - D) with D_i = rowsum(dO_i o O_i),
 //   dQ = scale dS K, dK = scale dS^T Q (dK, dV summed over the q-heads of a group).
 //
-// Three launches, no atomics:
-//  1. bwd_pre:  D and the log2-domain LSE in a tile-major workspace layout
-//               (a q-tile's 128 values form one aligned 512 B bulk copy).
+// Launches (after the tile map), no atomics:
+//  1. zero + bwd_pre: D and the log2-domain LSE in a tile-major workspace
+//               layout (a q-tile's 128 values form one aligned 512 B bulk copy).
 //  2. dkdv:     one CTA per (k-tile, sequence, kv head), visiting only the
 //               q-tiles of the tile map's column list (EMPTY tiles never
 //               loaded), for every q-head of the group.  K, V stay in smem;
-//               Q, dO, LSE, D stream through a 2-stage TMA ring.  TMEM:
-//               S^T [0,128), dP^T [128,256), dV, dK accumulators.  P^T (bf16)
-//               overwrites S^T in place and feeds dV += P^T dO from TMEM; dS^T
-//               (bf16) goes to smem and feeds dK += dS^T Q.  MMA order per
-//               iteration: dV(i), dP^T(i+1), S^T(i+1), dK(i) (in two K-halves)
-//               so the compute of i+1 overlaps dK(i).
-//  3. dq:       one CTA per (q-tile, sequence, q-head), visiting the tile map's
-//               row list: S = QK^T (double-buffered in TMEM), dP = dO V^T,
-//               dS (bf16) overwrites S and feeds dQ += dS K from TMEM.  The
-//               compute of tile j overlaps S(j+1) and dQ(j-1).
+//               Q, dO stream through a 5-slot TMA ring, LSE / D through a
+//               2-slot bulk-copy ring.  TMEM: S^T, dP^T, dV, dK (512 columns).
+//               P^T and dS^T (bf16) go back over the dP^T columns just read,
+//               in two halves, and feed dV += P^T dO and dK += dS^T Q as TS
+//               MMAs.  Issue order: S^T(i+1) once phase 1 has read S^T(i);
+//               the even k-steps of dV(i), dK(i) at the first half, the odd
+//               ones at the second; dP^T(i+1) right behind them.
+//  3. dq:       persistent, one CTA per SM walking (q-tile, sequence, q-head)
+//               units over the tile map's row lists: S = QK^T (double-
+//               buffered in TMEM), dP = dO V^T, dS (bf16) over S feeds
+//               dQ += dS K from TMEM; K through 4 slots, V through 1.  The
+//               pipelines run across units (next Q / dO load once the last S
+//               and dP of a unit are issued).
 // dQ is therefore accumulated in TMEM and written once (deterministic), at
 // the price of recomputing S and dP per (q-tile, k-tile) pair -- cheaper on
 // B200 than 64 KB of fp32 L2 reductions per tile pair (profiles/r01).
-// Compute warps: two warpgroups split the 128 columns of a tile; a thread owns
-// one TMEM lane (a key row in dkdv, a query row in dq).
+// Compute warps: four warpgroups split the 128 columns of a tile; a thread
+// owns one TMEM lane (a key row in dkdv, a query row in dq).
 #include "sm100.cuh"
 #include "tma_host.h"
 #include "tilemap.cuh"
