@@ -163,7 +163,7 @@ __device__ __forceinline__ void store_row_bf16_n(__nv_bfloat16* dst, const uint3
 #define BD_DKDV_POLY_MOD 0
 #endif
 #ifndef BD_DQ_POLY_MOD
-#define BD_DQ_POLY_MOD 0
+#define BD_DQ_POLY_MOD 4
 #endif
 
 template <int MOD>
