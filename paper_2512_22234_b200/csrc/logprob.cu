@@ -220,7 +220,10 @@ __global__ void __launch_bounds__(kThreads) logprob_bwd_kernel(int64_t n_rows, i
 // one HBM write of the logits (the two-kernel path reads them twice).
 // Requires V % (8 kCl) == 0 and 16-byte aligned rows (Qwen3 V = 151,936 is).
 constexpr int kCl = 4;
-constexpr int kFusedThreads = 256;
+#ifndef BD_LP_THREADS
+#define BD_LP_THREADS 256
+#endif
+constexpr int kFusedThreads = BD_LP_THREADS;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
