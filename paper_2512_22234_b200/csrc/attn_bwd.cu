@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
                          const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                          const BwdArgs a) {
   using C = DkdvCfg<D>;
+  const long long t_entry = (a.trace == 3 && threadIdx.x == 0) ? gtimer() : 0;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sK = smem + C::kOffK;
   uint8_t* sV = smem + C::kOffV;
@@ -570,6 +571,13 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<C::kTmemCols>(tbase);
+  if (a.trace == 3 && threadIdx.x == 0 && blockIdx.x < 32768) {  // BD_TRACE=3: per-CTA timeline
+    long long* e = g_cta_tl + 4 * blockIdx.x;
+    e[0] = t_entry;
+    e[1] = gtimer();
+    e[2] = n_it;
+    e[3] = smid();
+  }
 }
 
 // ===================================================================== dQ
