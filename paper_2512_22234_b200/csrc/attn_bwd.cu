@@ -162,6 +162,9 @@ __device__ __forceinline__ void store_row_bf16_n(__nv_bfloat16* dst, const uint3
 #ifndef BD_DKDV_POLY_MOD
 #define BD_DKDV_POLY_MOD 0
 #endif
+#ifndef BD_DKDV_TAIL_GROUPS
+#define BD_DKDV_TAIL_GROUPS 4
+#endif
 #ifndef BD_DQ_POLY_MOD
 #define BD_DQ_POLY_MOD 4
 #endif
@@ -275,9 +278,24 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
   if ((smem_u32(smem) & 1023u) != 0) __trap();
 
   // Grid order: (sequence, kv head) outermost, LPT rank of the k-tile inner --
-  // concurrently resident CTAs stream the same Q / dO tiles (L2 reuse).
-  const int unit = blockIdx.x / gm.NT;
-  const int rank = blockIdx.x - unit * gm.NT;
+  // concurrently resident CTAs stream the same Q / dO tiles (L2 reuse).  The
+  // last BD_DKDV_TAIL_GROUPS groups are merged into one LPT order (their
+  // ranks interleaved) so their longest columns start early enough not to
+  // leave a tail (list-scheduling model and BD_TRACE=3 timeline: 1.5% tail).
+  int unit, rank;
+  {
+    const int n_units = (int)(gridDim.x / gm.NT);
+    const int kt = n_units < BD_DKDV_TAIL_GROUPS ? n_units : BD_DKDV_TAIL_GROUPS;
+    const int split = (n_units - kt) * gm.NT;
+    if ((int)blockIdx.x < split || kt <= 1) {
+      unit = blockIdx.x / gm.NT;
+      rank = blockIdx.x - unit * gm.NT;
+    } else {
+      const int t = blockIdx.x - split;
+      rank = t / kt;
+      unit = n_units - kt + (t - rank * kt);
+    }
+  }
   const int mi = unit / a.n_kv_heads;  // map slot (varlen: longest sequences first)
   const int kvh = unit - mi * a.n_kv_heads;
   const int* mapb = VARLEN ? a.map + (size_t)mi * a.map_stride : a.map;
