@@ -623,9 +623,13 @@ struct DqCfg {
   static constexpr int kOffRing = 2 * kTileBytes;
   static constexpr int kOffBar = kOffRing + kStages * kTileBytes;
   // q_full, kv_full[S], kv_empty[S], s_full[2], dp_full, dp_free, compute_done[2], acc_full,
-  // qdo_empty, acc_empty
-  static constexpr int kNumBars = 1 + 2 * kStages + 9;
-  static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16;
+  // qdo_empty, acc_empty, unit_full[2], unit_empty[2]
+  static constexpr int kNumBars = 1 + 2 * kStages + 13;
+  // unit ring (2 slots): the TMA warp publishes each unit's decoded
+  // descriptor (128 B) and its rows' -log2 LSE and -D (2 x 512 B, bulk copy)
+  static constexpr int kOffUnit = (kOffBar + kNumBars * 8 + 16 + 127) / 128 * 128;
+  static constexpr int kSmemBytes = kOffUnit + 2 * 128 + 2 * 1024;
+  static_assert(kSmemBytes <= 232448, "dq smem budget");
 };
 
 // ring index 2j = K(j), 2j+1 = V(j)
@@ -650,8 +654,8 @@ __device__ __forceinline__ uint32_t dq_ring_phase(int idx) {
 // kernel).  Q / dO of unit u+1 load as soon as the last S and dP MMAs of unit
 // u are issued; the first dQ MMA of unit u+1 waits for the compute warps to
 // have drained unit u's accumulator from TMEM.
-struct DqUnit {
-  int b, h, qt, n_kt, q0, q1, qseg;
+struct __align__(128) DqUnit {  // one 128 B slot of the unit ring
+  int b, h, qt, n_kt, q0, q1, qseg, u;
   const int* ents;
   Geom g;
   bool valid;
@@ -669,6 +673,7 @@ __device__ __forceinline__ DqUnit dq_unit(const BwdArgs& a, int u) {
   const int kvh = unit - mi * a.n_kv_heads;
   r.h = kvh * a.group + (rem - rank * a.group);
   const int* mapb = VARLEN ? a.map + (size_t)mi * a.map_stride : a.map;
+  r.u = u;
   r.b = VARLEN ? map_seq(mapb) : mi;
   r.g = VARLEN ? map_geom(mapb) : gm;
   r.valid = !(VARLEN && rank >= r.g.NT);
@@ -709,7 +714,12 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
   uint64_t* acc_full = compute_done + 2;
   uint64_t* qdo_empty = acc_full + 1;  // last S, dP of a unit done: Q / dO reusable
   uint64_t* acc_empty = qdo_empty + 1;  // compute warps drained dQ from TMEM
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* unit_full = acc_empty + 1;   // [2] descriptor + LSE / D of a unit published
+  uint64_t* unit_empty = unit_full + 2;  // [2] read by the MMA thread and the 16 compute warps
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(unit_empty + 2);
+  DqUnit* udesc = reinterpret_cast<DqUnit*>(smem + C::kOffUnit);           // [2], 128 B apart
+  float* uvec = reinterpret_cast<float*>(smem + C::kOffUnit + 2 * 128);    // [2][256]
+  static_assert(sizeof(DqUnit) <= 128, "unit descriptor slot");
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if ((smem_u32(smem) & 1023u) != 0) __trap();
@@ -730,6 +740,10 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
     mbar_init(acc_full, 1);
     mbar_init(qdo_empty, 1);
     mbar_init(acc_empty, C::kComputeWarps);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&unit_full[t], 1);
+      mbar_init(&unit_empty[t], C::kComputeWarps + 1);
+    }
     fence_barrier_init();
   }
   tc_fence_before();
@@ -741,9 +755,25 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
     // ================================================================ TMA
     if (elect_one()) {
       int jg = 0, uu = 0;  // tiles and units this CTA has issued
+      // publication uu of the unit ring: slot uu & 1; a descriptor with
+      // valid = false ends the stream
+      auto publish = [&](const DqUnit& w, int pu) {
+        const int sl = pu & 1;
+        mbar_wait(&unit_empty[sl], (uint32_t)(((pu >> 1) & 1) ^ 1));
+        udesc[sl] = w;
+        if (w.valid) {
+          mbar_expect_tx(&unit_full[sl], 1024);
+          const size_t v0 = (((size_t)w.b * a.n_q_heads + w.h) * a.g.NT + w.qt) * kTileRows;
+          bulk_load(uvec + sl * 256, a.lse2_t + v0, 512, &unit_full[sl]);
+          bulk_load(uvec + sl * 256 + 128, a.dsum_t + v0, 512, &unit_full[sl]);
+        } else {
+          mbar_arrive(&unit_full[sl]);
+        }
+      };
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const DqUnit w = dq_unit<VARLEN>(a, u);
         if (!w.valid) continue;
+        publish(w, uu);
         const int kvh = w.h / a.group;
         mbar_wait(qdo_empty, (uint32_t)((uu & 1) ^ 1));
         mbar_expect_tx(q_full, 2 * C::kTileBytes);
@@ -764,6 +794,11 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
           }
         }
         ++uu;
+      }
+      {
+        DqUnit end = {};
+        end.valid = false;
+        publish(end, uu);
       }
       if (uu > 0) mbar_wait(qdo_empty, (uint32_t)((uu - 1) & 1));  // observe the last unit's release
     }
@@ -798,10 +833,13 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         umma_commit(&kv_empty[slot(2 * jg + 1)]);  // V consumed
       };
       int jb = 0, uu = 0;  // first global tile of the unit, units done
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const DqUnit w = dq_unit<VARLEN>(a, u);
-        if (!w.valid) continue;
-        const int n = w.n_kt;
+      for (;; ) {
+        const int sl = uu & 1;
+        mbar_wait(&unit_full[sl], (uint32_t)((uu >> 1) & 1));
+        const bool valid = udesc[sl].valid;
+        const int n = udesc[sl].n_kt;
+        mbar_arrive(&unit_empty[sl]);
+        if (!valid) break;
         mbar_wait(q_full, (uint32_t)(uu & 1));
         mbar_wait(&kv_full[slot(2 * jb)], ph(2 * jb));
         tc_fence_after();
@@ -854,19 +892,23 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
     const float sl2 = a.scale_log2;
     const int cb = wg * 32;
     int jg = 0, uu = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      const DqUnit w = dq_unit<VARLEN>(a, u);
-      if (!w.valid) continue;
+    for (;; ) {
+      const int sl = uu & 1;
+      mbar_wait(&unit_full[sl], (uint32_t)((uu >> 1) & 1));
+      const DqUnit w = udesc[sl];
+      if (!w.valid) break;
       const long long t_unit = (a.trace == 2 && threadIdx.x == 0) ? gtimer() : 0;
+      const float nlse2 = uvec[sl * 256 + r];  // -lse2 and -D (negated by bwd_pre)
+      const float ndsum = uvec[sl * 256 + 128 + r];
+      int ent_next = w.ents[0];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&unit_empty[sl]);
+      const int u = w.u;
       const Geom& g = w.g;
       const int row = w.q0 + r;
       int lo0, hi0, lo1, hi1;
       row_interval(g, w.qseg, row, 0, lo0, hi0);
       row_interval(g, w.qseg, row, w.qseg ? w.qseg : 1, lo1, hi1);  // the row's own noisy copy
-      const size_t vslot = (((size_t)w.b * a.n_q_heads + w.h) * a.g.NT + w.qt) * kTileRows + r;
-      const float nlse2 = a.lse2_t[vslot];
-      const float ndsum = a.dsum_t[vslot];
-      int ent_next = w.ents[0];
       for (int j = 0; j < w.n_kt; ++j, ++jg) {
         const int ent = ent_next;
         if (j + 1 < w.n_kt) ent_next = w.ents[j + 1];
