@@ -332,6 +332,15 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
     mbar_init(acc_done, 1);
     mbar_init(pt_half, C::kComputeWarps);
     fence_barrier_init();
+    // K, V loads go out before the CTA-wide barrier and the TMEM allocation
+    // (only this thread uses kv_full before the barrier)
+    if (n_it > 0) {
+      mbar_expect_tx(kv_full, 2 * C::kTileBytes);
+      for (int kb = 0; kb < D / 64; ++kb) {
+        tma_load_4d(sK + kb * 16384, &tmK, kv_full, kb * 64, kvh, k0, b);
+        tma_load_4d(sV + kb * 16384, &tmV, kv_full, kb * 64, kvh, k0, b);
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -341,11 +350,6 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
   if (warp == C::kTmaWarp) {
     // ================================================================ TMA
     if (elect_one() && n_it > 0) {
-      mbar_expect_tx(kv_full, 2 * C::kTileBytes);
-      for (int kb = 0; kb < D / 64; ++kb) {
-        tma_load_4d(sK + kb * 16384, &tmK, kv_full, kb * 64, kvh, k0, b);
-        tma_load_4d(sV + kb * 16384, &tmV, kv_full, kb * 64, kvh, k0, b);
-      }
       // LSE / D vectors one iteration ahead of Q / dO: vec(i+1) is issued right
       // after dO(i) (its 2-slot ring frees a whole iteration earlier than the
       // Q / dO slots), so its ~1 us load latency is off the compute path

@@ -222,9 +222,14 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
       mbar_init(&p_half[q], 4);
     }
     fence_barrier_init();
-    tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
+    // Q goes out before the CTA-wide barrier and the TMEM allocation (only
+    // this thread uses q_full before the barrier)
+    mbar_expect_tx(q_full, NQ * C::kTileBytes);
+    for (int q = 0; q < NQ; ++q)
+      for (int kb = 0; kb < D / 64; ++kb)
+        tma_load_4d(sQ + q * C::kTileBytes + kb * 16384, &tmQ, q_full, kb * 64, h0 + q, q0, b);
   }
   tc_fence_before();
   __syncthreads();
@@ -234,10 +239,6 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
   if (warp == C::kTmaWarp) {
     // ================================================================ TMA
     if (elect_one()) {
-      mbar_expect_tx(q_full, NQ * C::kTileBytes);
-      for (int q = 0; q < NQ; ++q)
-        for (int kb = 0; kb < D / 64; ++kb)
-          tma_load_4d(sQ + q * C::kTileBytes + kb * 16384, &tmQ, q_full, kb * 64, h0 + q, q0, b);
       int stage = 0;
       uint32_t phase = 0;
       for (int j = 0; j < n_kt; ++j) {
