@@ -113,9 +113,30 @@ __device__ int classify_pair_warp(const Geom& g, int qt, int kt, const int* s_lo
   return any ? (all ? kKindFull : kKindPartial) : 0;
 }
 
+#ifndef BD_MAP_TRACE
+#define BD_MAP_TRACE 0
+#endif
+#if BD_MAP_TRACE
+__device__ long long g_map_trace[16];
+#define MAP_STAMP(i) \
+  do {               \
+    __syncthreads(); \
+    if (threadIdx.x == 0 && blockIdx.x == 0) g_map_trace[i] = clock64(); \
+  } while (0)
+#else
+#define MAP_STAMP(i) \
+  do {               \
+  } while (0)
+#endif
+
 // One warp per q-tile (strided).  Shared memory: rowlen[NT], collen[NT],
 // colfill[NT], scan scratch[1024], and per warp 4 x 128 ints of row intervals.
-__device__ void build_map_body(const Geom& g, int* __restrict__ ws, int seq) {
+// stage != 0 (the map fits): pass 1 also keeps every row's entries in shared
+// memory (fixed stride cap / NT per q-tile), so the fill pass copies them
+// instead of classifying every candidate a second time, and pass 3 reads
+// entries and column pointers from shared memory (BD_MAP_TRACE: the two
+// classification passes were ~85% of the builder's time).
+__device__ void build_map_body(const Geom& g, int* __restrict__ ws, int seq, int stage) {
   extern __shared__ int sh[];
   const int NT = g.NT;
   int* rowlen = sh;                 // NT
@@ -125,7 +146,11 @@ __device__ void build_map_body(const Geom& g, int* __restrict__ ws, int seq) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = kBuildThreads / 32;
   int* wiv = sh + 3 * NT + kBuildThreads + warp * 512;  // this warp's row intervals
   const int cap = map_capacity(g);
+  const int stride = cap / NT;  // per-q-tile entry bound (T0 + own-copy tiles)
+  int* s_cp = sh + 3 * NT + kBuildThreads + (kBuildThreads / 32) * 512;  // stage: col_ptr[NT + 1]
+  int* s_ent = s_cp + NT + 1;                                              // stage: [NT][stride]
   MapView mv{ws, NT, cap};
+  MAP_STAMP(0);
   for (int i = tid; i < NT; i += kBuildThreads) {
     collen[i] = 0;
     colfill[i] = 0;
@@ -133,6 +158,21 @@ __device__ void build_map_body(const Geom& g, int* __restrict__ ws, int seq) {
   __syncthreads();
   // passes 1 and 2: classify candidate k-tiles of each q-tile; count, then fill
   for (int pass = 0; pass < 2; ++pass) {
+    if (pass && stage) {
+      // fill from the entries kept by pass 1
+      for (int t = warp; t < NT; t += nwarps) {
+        const int r0 = mv.row_ptr()[t], n = rowlen[t];
+        for (int i = lane; i < n; i += 32) {
+          const int e = s_ent[t * stride + i];
+          mv.row_ent()[r0 + i] = e;
+          atomicAdd(&collen[entry_tile(e)], 1);
+        }
+      }
+      __syncthreads();
+      MAP_STAMP(3);
+      MAP_STAMP(4);
+      break;
+    }
     for (int t = warp; t < NT; t += nwarps) {
       const int q0 = tile_start(g, t), nrow = tile_end(g, t) - q0, qs = tile_seg(g, t);
       for (int r = lane; r < nrow; r += 32) {
@@ -141,6 +181,39 @@ __device__ void build_map_body(const Geom& g, int* __restrict__ ws, int seq) {
       }
       __syncwarp();
       int n = pass ? mv.row_ptr()[t] : 0;
+      if (!pass) {
+        // count (and, staged, keep) the row's entries: lane i classifies
+        // candidate base + i over all rows of the tile (broadcast reads of the
+        // row intervals), a ballot keeps the entries in increasing k-tile order
+        for (int kk = 0; kk < (qs ? 2 : 1); ++kk) {
+          const int ks = kk ? qs : 0;  // x0, then the row's own copy
+          int a, b;
+          candidate_range(g, t, ks, a, b);
+          const int* s_lo = wiv + 256 * kk;
+          const int* s_hi = s_lo + 128;
+          for (int base = a; base < b; base += 32) {
+            const int kt = base + lane;
+            int kind = 0;
+            if (kt < b) {
+              const int k0 = tile_start(g, kt), k1 = tile_end(g, kt);
+              bool any = false, all = true;
+#pragma unroll 8
+              for (int r = 0; r < nrow; ++r) {
+                const int lo = max(s_lo[r], k0), hi = min(s_hi[r], k1);
+                any |= hi > lo;
+                all &= (lo == k0 && hi == k1);
+              }
+              kind = any ? (all ? kKindFull : kKindPartial) : 0;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, kind != 0);
+            if (stage && kind) s_ent[t * stride + n + __popc(m & ((1u << lane) - 1u))] = entry_make(kt, kind);
+            n += __popc(m);
+          }
+        }
+        if (lane == 0) rowlen[t] = n;
+        __syncwarp();
+        continue;
+      }
       for (int kk = 0; kk < (qs ? 2 : 1); ++kk) {
         const int ks = kk ? qs : 0;  // x0, then the row's own copy
         int a, b;
@@ -148,7 +221,7 @@ __device__ void build_map_body(const Geom& g, int* __restrict__ ws, int seq) {
         for (int kt = a; kt < b; ++kt) {
           const int kind = classify_pair_warp(g, t, kt, wiv + 256 * kk, wiv + 256 * kk + 128);
           if (kind) {
-            if (pass && lane == 0) {
+            if (lane == 0) {
               mv.row_ent()[n] = entry_make(kt, kind);
               atomicAdd(&collen[kt], 1);
             }
@@ -156,26 +229,42 @@ __device__ void build_map_body(const Geom& g, int* __restrict__ ws, int seq) {
           }
         }
       }
-      if (!pass && lane == 0) rowlen[t] = n;
       __syncwarp();
     }
     __syncthreads();
+    MAP_STAMP(1 + 2 * pass);
     if (!pass) block_exclusive_scan(rowlen, mv.row_ptr(), NT, scratch);
+    MAP_STAMP(2 + 2 * pass);
   }
   block_exclusive_scan(collen, mv.col_ptr(), NT, scratch);
+  MAP_STAMP(5);
+  if (stage) {
+    for (int i = tid; i <= NT; i += kBuildThreads) s_cp[i] = mv.col_ptr()[i];
+    __syncthreads();
+  }
   // pass 3: column entries in increasing q-tile order -- warp 0 walks the rows
   // in order, lanes take a row's entries (each k-tile appears once per row)
   if (warp == 0) {
     for (int t = 0; t < NT; ++t) {
-      const int e0 = mv.row_ptr()[t], e1 = mv.row_ptr()[t + 1];
-      for (int e = e0 + lane; e < e1; e += 32) {
-        const int ent = mv.row_ent()[e];
-        const int kt = entry_tile(ent);
-        mv.col_ent()[mv.col_ptr()[kt] + colfill[kt]++] = entry_make(t, entry_kind(ent));
+      if (stage) {
+        const int n = rowlen[t];
+        for (int i = lane; i < n; i += 32) {
+          const int ent = s_ent[t * stride + i];
+          const int kt = entry_tile(ent);
+          mv.col_ent()[s_cp[kt] + colfill[kt]++] = entry_make(t, entry_kind(ent));
+        }
+      } else {
+        const int e0 = mv.row_ptr()[t], e1 = mv.row_ptr()[t + 1];
+        for (int e = e0 + lane; e < e1; e += 32) {
+          const int ent = mv.row_ent()[e];
+          const int kt = entry_tile(ent);
+          mv.col_ent()[mv.col_ptr()[kt] + colfill[kt]++] = entry_make(t, entry_kind(ent));
+        }
       }
       __syncwarp();
     }
   }
+  MAP_STAMP(6);
   // pass 4: longest-first orders (stable: ties by index)
   for (int t = tid; t < NT; t += kBuildThreads) {
     const int lt = rowlen[t], ct = collen[t];
@@ -189,6 +278,7 @@ __device__ void build_map_body(const Geom& g, int* __restrict__ ws, int seq) {
     mv.bwd_order()[rc] = t;
   }
   __syncthreads();
+  MAP_STAMP(7);
   if (tid == 0) {
     int maxrow = 0;
     for (int t = 0; t < NT; ++t) maxrow = max(maxrow, rowlen[t]);
@@ -205,40 +295,51 @@ __device__ void build_map_body(const Geom& g, int* __restrict__ ws, int seq) {
   }
 }
 
-__global__ void __launch_bounds__(kBuildThreads, 1) build_map_kernel(Geom g, int* __restrict__ ws) {
-  build_map_body(g, ws, 0);
+__global__ void __launch_bounds__(kBuildThreads, 1) build_map_kernel(Geom g, int* __restrict__ ws, int stage) {
+  build_map_body(g, ws, 0, stage);
 }
 
 // Varlen: CTA i builds sequence i's map at ws + i * stride.
 __global__ void __launch_bounds__(kBuildThreads, 1)
-    build_map_varlen_kernel(const __grid_constant__ SeqLens lens, int* __restrict__ ws, long long stride) {
-  build_map_body(seq_geom(lens, blockIdx.x), ws + blockIdx.x * stride, lens.seq[blockIdx.x]);
+    build_map_varlen_kernel(const __grid_constant__ SeqLens lens, int* __restrict__ ws, long long stride, int stage) {
+  build_map_body(seq_geom(lens, blockIdx.x), ws + blockIdx.x * stride, lens.seq[blockIdx.x], stage);
+}
+
+// Dynamic shared memory of the builder; the staged layout if it fits in 227 KB
+// (varlen: sized for the longest sequence, whose map bounds every other one).
+size_t build_smem(const Geom& g, int& stage) {
+  const size_t base = (3 * (size_t)g.NT + kBuildThreads + (kBuildThreads / 32) * 512) * sizeof(int);
+  const size_t staged = base + ((size_t)g.NT + 1 + (size_t)map_capacity(g)) * sizeof(int);
+  stage = staged <= 227 * 1024 ? 1 : 0;
+  return stage ? staged : base;
 }
 
 }  // namespace
 
 int build_map_device(const Geom& g, int* ws, cudaStream_t stream) {
-  const size_t smem = (3 * (size_t)g.NT + kBuildThreads + (kBuildThreads / 32) * 512) * sizeof(int);
+  int stage = 0;
+  const size_t smem = build_smem(g, stage);
   if (g.NT > kMaxTiles) return set_error(BD_ERR_UNSUPPORTED, "too many tiles (%d > %d)", g.NT, kMaxTiles);
   static bool attr_done = false;
   if (!attr_done) {
     cudaFuncSetAttribute(build_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_done = true;
   }
-  build_map_kernel<<<1, kBuildThreads, smem, stream>>>(g, ws);
+  build_map_kernel<<<1, kBuildThreads, smem, stream>>>(g, ws, stage);
   note_launches(1);
   return check_cuda(cudaGetLastError(), "build_map_kernel launch");
 }
 
 int build_map_device_varlen(const Geom& gmax, const SeqLens& lens, int* ws, long long stride, cudaStream_t stream) {
-  const size_t smem = (3 * (size_t)gmax.NT + kBuildThreads + (kBuildThreads / 32) * 512) * sizeof(int);
+  int stage = 0;
+  const size_t smem = build_smem(gmax, stage);
   if (gmax.NT > kMaxTiles) return set_error(BD_ERR_UNSUPPORTED, "too many tiles (%d > %d)", gmax.NT, kMaxTiles);
   static bool attr_done = false;
   if (!attr_done) {
     cudaFuncSetAttribute(build_map_varlen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_done = true;
   }
-  build_map_varlen_kernel<<<lens.n, kBuildThreads, smem, stream>>>(lens, ws, stride);
+  build_map_varlen_kernel<<<lens.n, kBuildThreads, smem, stream>>>(lens, ws, stride, stage);
   note_launches(1);
   return check_cuda(cudaGetLastError(), "build_map_varlen_kernel launch");
 }
@@ -332,3 +433,10 @@ extern "C" int bd_tilemap_selfcheck(const bd_problem* prob, int64_t* mismatches)
   *mismatches = bad;
   return BD_OK;
 }
+
+#if BD_MAP_TRACE
+extern "C" int bd_debug_map_trace(int64_t* host_out, int n) {
+  if (!host_out || n <= 0 || n > 16) return BD_ERR_INVALID_ARG;
+  return bd::check_cuda(cudaMemcpyFromSymbol(host_out, bd::g_map_trace, n * sizeof(long long)), "map trace copy");
+}
+#endif
