@@ -368,6 +368,12 @@ def run_ours(args):
         "pct_bf16_peak_burst": round(value / world / peak_b * 100, 2),
         "peak_source": peak_src,
         "tokens_per_s": round(world * tokens_step / (ms * 1e-3), 1),
+        # also response tokens/s of the step and the fused
+        # logprob's rows/s inside it (its own phase time)
+        "response_tokens_per_s": round(world * (sum(cfg.resp_lens) if cfg.resp_lens else cfg.batch * cfg.response_len)
+                                       / (ms * 1e-3), 1),
+        "logprob_rows_per_s": (round(world * step.n_rows / (phase["logprob_fused"] * 1e-3), 1)
+                               if phase.get("logprob_fused") else None),
         "phase_ms": {k: round(v, 3) for k, v in phase.items()},
         "dipo_loss": loss_val,
         "roofline": roofline,
