@@ -245,10 +245,20 @@ def run_ours(args):
     # read back D2H; the copy of step i+1 runs on a side stream into the second
     # of two device input buffers while step i computes (double buffering).
     e2e = None
-    if not args.no_e2e:
+    e2e_ok = not args.no_e2e
+    if e2e_ok:
         names = ("q", "k", "v", "do", "targets", "rewards")
-        host = {n: torch.empty(getattr(step, n).shape, dtype=getattr(step, n).dtype, pin_memory=True)
-                for n in names}
+        try:  # pinned host inputs (~6 GB per rank at SDAR-8B); agreed across ranks before any collective
+            host = {n: torch.empty(getattr(step, n).shape, dtype=getattr(step, n).dtype, pin_memory=True)
+                    for n in names}
+        except Exception as ex:  # noqa: BLE001 -- reported, the device-resident line still prints
+            print(f"[bench] e2e skipped: pinned host allocation failed: {ex}", file=sys.stderr)
+            e2e_ok = False
+        if world > 1:
+            flag = torch.tensor([1 if e2e_ok else 0], device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            e2e_ok = bool(flag.item())
+    if e2e_ok:
         for n, h in host.items():
             h.copy_(getattr(step, n))
         bufs = [{n: getattr(step, n) for n in names}, {n: torch.empty_like(getattr(step, n)) for n in names}]
