@@ -25,6 +25,12 @@ CASES = [
     ("copies3_resp_only_ragged", AttnConfig("t2", 1, 2, 1, 128, 40, 200, 8, repeat_prompt=0, n_copies=3)),
     ("copies4_d64_B1", AttnConfig("t3", 1, 2, 2, 64, 0, 136, 1, n_copies=4)),
     ("copies2_B128", AttnConfig("t4", 1, 2, 1, 128, 128, 256, 128, n_copies=2)),
+    # more dQ units than SMs: the persistent dQ kernel walks several units per
+    # CTA (unit ring slot reuse, Q / dO reload, accumulator drain between
+    # units); 16 / 12 (sequence, kv head) groups exercise the merged LPT tail
+    # of the dK/dV grid
+    ("many_units_d64", AttnConfig("m1", 8, 8, 2, 64, 64, 320, 4)),
+    ("many_units_d128", AttnConfig("m2", 6, 8, 2, 128, 32, 352, 8)),
 ]
 
 
