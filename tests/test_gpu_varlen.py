@@ -22,6 +22,10 @@ CASES = [
     ("resp_only_ragged", 2, 1, 128, 8, 0, 1, [(40, 200), (16, 48), (40, 8)]),
     ("copies2_d64", 2, 2, 64, 4, 1, 2, [(16, 176), (8, 40), (16, 112)]),
     ("single_seq", 4, 2, 128, 4, 1, 1, [(32, 96)]),
+    # more dQ units than SMs with many skipped (short sequences): the
+    # persistent dQ kernel's publisher skips units past a sequence's tile count
+    ("many_seqs_units", 8, 2, 64, 4, 1, 1,
+     [(64, 448), (8, 24), (32, 160), (0, 512), (16, 80), (64, 320), (24, 40), (48, 208), (0, 96), (40, 472)]),
 ]
 
 
