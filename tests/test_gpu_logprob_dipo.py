@@ -125,3 +125,33 @@ def test_dipo_online_rho_one(cuda_ok):
     torch.cuda.synchronize()
     assert abs(gloss.item() - loss) < 1e-9
     np.testing.assert_allclose(t2np(gdl), dl, rtol=1e-6, atol=1e-9)
+
+
+@pytest.mark.gpu
+def test_fused_logprob_masked_vocab(cuda_ok):
+    """-inf logits (masked vocabulary entries) through the one-barrier fused
+    kernel: a whole cluster slice masked (its (max, sum) pair is (-inf, 0)), the
+    slice holding the row max masked, half the vocabulary masked at random;
+    targets stay on finite entries.  Masked entries get dz = 0 exactly."""
+    n, V = 4, VOCAB_QWEN3
+    z, t = logits_inputs(n, V, seed=21)
+    q = V // 4  # the fused kernel's slice per CTA of the 4-CTA cluster
+    z[0, :q] = float("-inf")
+    z[1, 2 * q:3 * q] = float("-inf")
+    g = torch.Generator().manual_seed(4)
+    z[2, torch.rand(V, generator=g) < 0.5] = float("-inf")
+    for i in range(n):  # targets on finite logits
+        while not torch.isfinite(z[i, t[i]]):
+            t[i] = (t[i] + 997) % V
+    w = torch.randn(n, generator=torch.Generator().manual_seed(6), dtype=torch.float32)
+    zc = z.cuda()
+    logp, lse, dz = ops.logprob(zc, t.cuda(), dlogp=w.cuda())
+    torch.cuda.synchronize()
+    ref_lp, ref_lse = olp.logprob(z, t.long())
+    ref_dz = olp.logprob_grad(z, t.long(), w.double().numpy())
+    assert metrics(t2np(logp), ref_lp)["max_abs"] <= LOGP_MAX_ABS
+    assert metrics(t2np(lse), ref_lse)["max_abs"] <= LOGP_MAX_ABS
+    d = t2np(dz)
+    assert np.isfinite(d).all()
+    assert (d[~np.isfinite(t2np(z))] == 0).all()
+    assert metrics(d, ref_dz)["rel_l2"] <= DZ_REL_L2
