@@ -90,6 +90,18 @@ typedef struct bd_problem {
    * into a kernel parameter, no host->device transfer); batch <= 1024.     */
   const int32_t* seq_prompt_len;
   const int32_t* seq_response_len;
+  /* Head sharding ((sequence, kv-head-group) units when there
+   * are fewer sequences than GPUs; north star "sequences and heads are
+   * partitioned"): the number of heads per token row IN MEMORY of the
+   * q / o / dout / dq tensors (q_row_heads) and of the k / v / dk / dv tensors
+   * (kv_row_heads); 0 = dense (n_q_heads / n_kv_heads).  A rank that owns kv
+   * heads [g0, g0 + n_kv_heads) of a model with Hkv_total kv heads passes
+   * k + g0 d, v + g0 d, ... and q + g0 (Hq/Hkv) d, ... with kv_row_heads =
+   * Hkv_total, q_row_heads = Hq_total: no copies.  Must be >= n_q_heads /
+   * n_kv_heads.  LSE stays a dense [b, n_q_heads, Ntot] buffer of the local
+   * heads.                                                                */
+  int32_t q_row_heads;
+  int32_t kv_row_heads;
 } bd_problem;
 
 /* Packed length Ntot of one sequence, or -1 if the problem is invalid. */
@@ -104,6 +116,7 @@ size_t bd_attn_workspace_bytes(const bd_problem* prob, int backward);
 /* Forward.
  *   q    bf16 [b, Ntot, Hq,  d]      k, v  bf16 [b, Ntot, Hkv, d]
  *   o    bf16 [b, Ntot, Hq,  d]      (written)
+ *        (row strides q_row_heads d / kv_row_heads d elements when set)
  *   lse  fp32 [b, Hq, Ntot]          natural-log log-sum-exp of the scaled,
  *                                    masked scores of each row (written)
  *   ws   device workspace of >= bd_attn_workspace_bytes(prob, 0) bytes.
@@ -216,11 +229,12 @@ int bd_decode_select(int32_t batch, int32_t block, int32_t vocab, const void* lo
 
 /* DiPO, step 1: per-group partial statistics of the local trajectories.
  *   rewards        fp32 [n_traj]       r_i
- *   group_of_traj  int32 [n_traj]      global group id in [0, n_groups)
+ *   group_of_traj  int32 [n_traj]      global group id in [0, n_groups); other ids are ignored
  *   traj_len       int32 [n_traj]      |tau_i| in tokens (reading c10)
  *   group_stats    fp64 [n_groups, 3]  += (sum r, count, sum |tau|)   (accumulated;
  *                                      zero it first; all-reduce(SUM) it across
- *                                      ranks when a group straddles ranks)  */
+ *                                      ranks when a group straddles ranks)
+ * Deterministic: each group's sums run in trajectory order (no atomics). */
 int bd_dipo_group_stats(int32_t n_traj, const float* rewards, const int32_t* group_of_traj,
                         const int32_t* traj_len, int32_t n_groups, double* group_stats, void* stream);
 
@@ -230,17 +244,22 @@ int bd_dipo_group_stats(int32_t n_traj, const float* rewards, const int32_t* gro
  *                                      the online setting of Eq. 7 (pi_old = sg(pi_theta)):
  *                                      rho == 1, so the weights are known before the
  *                                      log-probs (enables the fused bd_logprob pass)
- *   traj_of_token  int32 [n_tokens]    local trajectory index
- *   rewards, group_of_traj             as in step 1 (local trajectories)
+ *   traj_of_token  int32 [n_tokens]    local trajectory index in [0, n_traj)
+ *   rewards, group_of_traj             as in step 1 (n_traj local trajectories)
  *   group_stats    fp64 [n_groups, 3]  globally reduced output of step 1
- *   n_groups_global                    number of non-empty groups overall
+ *   n_groups_global                    number of non-empty groups overall (the 1/n_groups
+ *                                      normaliser; reading c11)
  *   eps                                clip range of C_eps
  *   dlogp          fp32 [n_tokens]     dloss/dlogp_k (written)
  *   partials       fp64 [3]            += (loss partial, tokens, clipped tokens)
- * A_i = r_i - mean_g r;  loss = -(1/n_groups) sum_g (1/N_g) sum C_eps(rho, A). */
+ * A_i = r_i - mean_g r;  loss = -(1/n_groups) sum_g (1/N_g) sum C_eps(rho, A).
+ * A token whose trajectory or group id is out of range, or whose group is
+ * empty, gets dlogp = NaN and makes the loss partial NaN ("abort").
+ * Deterministic: the partials are summed by one CTA in a fixed order. */
 int bd_dipo_token_loss(int64_t n_tokens, const float* logp, const float* logp_old, const int32_t* traj_of_token,
-                       const float* rewards, const int32_t* group_of_traj, const double* group_stats,
-                       int32_t n_groups_global, float eps, float* dlogp, double* partials, void* stream);
+                       int32_t n_traj, const float* rewards, const int32_t* group_of_traj, const double* group_stats,
+                       int32_t n_groups, int32_t n_groups_global, float eps, float* dlogp, double* partials,
+                       void* stream);
 
 /* Tile map (host path, for tests).  Writes the ordered list of non-empty
  * 128x128 tiles as 5-tuples (q_seg, q_tile, k_seg, k_tile, kind) of int32
@@ -258,6 +277,17 @@ int bd_tilemap_stats(const bd_problem* prob, int64_t* out);
  * kernel describe the same mask for every (row, key); *mismatches (host)
  * receives the count (0 expected).  Small problems only (Ntot^2 <= 2^26). */
 int bd_tilemap_selfcheck(const bd_problem* prob, int64_t* mismatches);
+
+/* Element mask (host, tests): the per-element visibility the kernels
+ * evaluate on PARTIAL and ragged tiles, for rows [row0, row0 + n_rows) of
+ * sequence `seq` (a varlen batch: that sequence's own lengths) and all of its
+ * *n_keys packed keys: host_out[i * n_keys + k] bit 0 = key k inside row
+ * row0 + i's visible interval (forward / dQ kernels), bit 1 = that row inside
+ * key k's visible-row interval (dK/dV kernel).  Must equal the dense mask of
+ * the rule ("bitmatrix and predicate agree everywhere").
+ * Returns BD_ERR_WORKSPACE if cap < n_rows * n_keys (n_keys is set). */
+int bd_mask_dump(const bd_problem* prob, int32_t seq, int64_t row0, int64_t n_rows, uint8_t* host_out, size_t cap,
+                 int64_t* n_keys);
 
 const char* bd_error_string(int code);
 const char* bd_last_error(void);

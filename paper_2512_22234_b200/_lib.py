@@ -27,6 +27,8 @@ class BdProblem(ctypes.Structure):
         ("n_copies", ctypes.c_int32),
         ("seq_prompt_len", ctypes.POINTER(ctypes.c_int32)),
         ("seq_response_len", ctypes.POINTER(ctypes.c_int32)),
+        ("q_row_heads", ctypes.c_int32),
+        ("kv_row_heads", ctypes.c_int32),
     ]
 
 
@@ -47,10 +49,11 @@ SIGNATURES = {
     "bd_logprob_bwd": (ctypes.c_int, [_I64, _I32, _P, _I64, _P, _P, _P, _P, _I64, _P]),
     "bd_launch_count": (_I64, []),
     "bd_dipo_group_stats":(ctypes.c_int, [_I32, _P, _P, _P, _I32, _P, _P]),
-    "bd_dipo_token_loss": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P, _I32, _F, _P, _P, _P]),
+    "bd_dipo_token_loss": (ctypes.c_int, [_I64, _P, _P, _P, _I32, _P, _P, _P, _I32, _I32, _F, _P, _P, _P]),
     "bd_tilemap_dump": (ctypes.c_int, [_PROB, ctypes.POINTER(_I32), _SZ, ctypes.POINTER(_I64)]),
     "bd_tilemap_stats": (ctypes.c_int, [_PROB, ctypes.POINTER(_I64)]),
     "bd_tilemap_selfcheck": (ctypes.c_int, [_PROB, ctypes.POINTER(_I64)]),
+    "bd_mask_dump": (ctypes.c_int, [_PROB, _I32, _I64, _I64, _P, _SZ, ctypes.POINTER(_I64)]),
     "bd_error_string": (ctypes.c_char_p, [ctypes.c_int]),
     "bd_last_error": (ctypes.c_char_p, []),
     "bd_selftest_mma": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),

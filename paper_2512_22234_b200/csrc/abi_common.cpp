@@ -4,6 +4,9 @@
 #include <cstdio>
 #include <cstdarg>
 #include <atomic>
+#include <mutex>
+#include <map>
+#include <utility>
 
 namespace bd {
 
@@ -23,6 +26,39 @@ int set_error(int code, const char* fmt, ...) {
 int check_cuda(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return BD_OK;
   return set_error(BD_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int ensure_smem_attr(const void* func, int bytes, const char* what) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;  // (function, device) -> bytes set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return check_cuda(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = done.find({func, dev});
+  if (it != done.end() && it->second >= bytes) return BD_OK;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return check_cuda(e, what);
+  done[{func, dev}] = bytes;
+  return BD_OK;
+}
+
+int current_sm_count(int* n_sm) {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return check_cuda(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it == cache.end()) {
+    int n = 0;
+    e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return check_cuda(e, "cudaDeviceGetAttribute(SM count)");
+    it = cache.emplace(dev, n).first;
+  }
+  *n_sm = it->second;
+  return BD_OK;
 }
 
 }  // namespace bd

@@ -51,7 +51,7 @@ template <int D, bool VARLEN>
 __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __restrict__ o,
                                                       const __nv_bfloat16* __restrict__ dout,
                                                       const float* __restrict__ lse, float* __restrict__ lse2_t,
-                                                      float* __restrict__ dsum_t, int N, int Hq, Geom gm,
+                                                      float* __restrict__ dsum_t, int N, int Hq, int q_rh, Geom gm,
                                                       const int* __restrict__ map, int map_stride) {
   constexpr int kTpr = D / 8;             // threads per row
   constexpr int kRows = 256 / kTpr;       // rows per block
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
   const bool valid = n < (VARLEN ? g.N : N);
   float acc = 0.f;
   if (valid) {
-    const size_t base = (((size_t)b * N + n) * Hq + h) * D + sub * 8;
+    const size_t base = (((size_t)b * N + n) * q_rh + h) * D + sub * 8;  // q_rh: heads per row in memory
     const uint4 a = *reinterpret_cast<const uint4*>(o + base);
     const uint4 c = *reinterpret_cast<const uint4*>(dout + base);
     const uint32_t av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
@@ -126,6 +126,7 @@ struct BwdArgs {
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
   int batch, n_q_heads, n_kv_heads, group, N;
+  int q_row_heads, kv_row_heads;  // heads per token row of dq / dk, dv in memory
   Geom g;
   float scale, scale_log2;
   int trace;  // 1 = record the trace for blockIdx.x == 0
@@ -570,7 +571,7 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
     }
     const bool ok = kpos < k1;
     constexpr int DC = D / C::kWGs;  // 32 (D = 128) or 16 (D = 64)
-    const size_t orow = (((size_t)b * a.N + kpos) * a.n_kv_heads + kvh) * D + wg * DC;
+    const size_t orow = (((size_t)b * a.N + kpos) * a.kv_row_heads + kvh) * D + wg * DC;
 #pragma unroll
     for (int which = 0; which < 2; ++which) {
       const uint32_t col = (which ? C::kColDK : C::kColDV) + wg * DC;
@@ -972,7 +973,7 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty);  // accumulator free for the next unit
-      __nv_bfloat16* out = a.dq + (((size_t)w.b * a.N + row) * a.n_q_heads + w.h) * D + wg * DC;
+      __nv_bfloat16* out = a.dq + (((size_t)w.b * a.N + row) * a.q_row_heads + w.h) * D + wg * DC;
       store_row_bf16_n<DC>(out, v, a.scale, row < w.q1);
       if (a.trace == 2 && threadIdx.x == 0 && u < 32768) {
         long long* e = g_cta_tl + 4 * u;
@@ -990,12 +991,8 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
 }
 
 template <typename K>
-int set_smem(K kernel, int bytes, bool& done) {
-  if (done) return BD_OK;
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(bwd)");
-  done = true;
-  return BD_OK;
+int set_smem(K kernel, int bytes) {
+  return ensure_smem_attr(reinterpret_cast<const void*>(kernel), bytes, "cudaFuncSetAttribute(bwd)");
 }
 
 template <int D, bool VARLEN>
@@ -1013,16 +1010,18 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
     dim3 grid((g.N + kRows - 1) / kRows, p.batch * Hq);
     bwd_pre_kernel<D, VARLEN><<<grid, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
                                                          reinterpret_cast<const __nv_bfloat16*>(dout), lse, lse2_t,
-                                                         dsum_t, g.N, Hq, g, map, map_stride);
+                                                         dsum_t, g.N, Hq, q_row_heads(p), g, map, map_stride);
   }
   CUtensorMap tmQ, tmK, tmV, tmDO;
-  if (!make_qkv_tmap(&tmQ, q, p.batch, g.N, Hq, D) || !make_qkv_tmap(&tmK, k, p.batch, g.N, p.n_kv_heads, D) ||
-      !make_qkv_tmap(&tmV, v, p.batch, g.N, p.n_kv_heads, D) || !make_qkv_tmap(&tmDO, dout, p.batch, g.N, Hq, D))
+  const int qrh = q_row_heads(p), kvrh = kv_row_heads(p);
+  if (!make_qkv_tmap(&tmQ, q, p.batch, g.N, Hq, D, 128, qrh) ||
+      !make_qkv_tmap(&tmK, k, p.batch, g.N, p.n_kv_heads, D, 128, kvrh) ||
+      !make_qkv_tmap(&tmV, v, p.batch, g.N, p.n_kv_heads, D, 128, kvrh) ||
+      !make_qkv_tmap(&tmDO, dout, p.batch, g.N, Hq, D, 128, qrh))
     return set_error(BD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  static bool attr_kv = false, attr_q = false;
-  int rc = set_smem(attn_bwd_dkdv_kernel<D, VARLEN>, DkdvCfg<D>::kSmemBytes, attr_kv);
+  int rc = set_smem(attn_bwd_dkdv_kernel<D, VARLEN>, DkdvCfg<D>::kSmemBytes);
   if (rc) return rc;
-  if ((rc = set_smem(attn_bwd_dqp_kernel<D, VARLEN>, DqCfg<D>::kSmemBytes, attr_q))) return rc;
+  if ((rc = set_smem(attn_bwd_dqp_kernel<D, VARLEN>, DqCfg<D>::kSmemBytes))) return rc;
   BwdArgs a;
   a.map = map;
   a.map_stride = map_stride;
@@ -1034,6 +1033,8 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   a.batch = p.batch;
   a.n_q_heads = Hq;
   a.n_kv_heads = p.n_kv_heads;
+  a.q_row_heads = qrh;
+  a.kv_row_heads = kvrh;
   a.group = Hq / p.n_kv_heads;
   a.N = g.N;
   a.g = g;
@@ -1049,12 +1050,8 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   // 3. dQ
   const long long grid_q = (long long)g.NT * p.batch * Hq;
   if (grid_q > 0x7FFFFFFF) return set_error(BD_ERR_UNSUPPORTED, "grid too large");
-  static int n_sm = 0;
-  if (!n_sm) {
-    int dev = 0;
-    if ((rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice"))) return rc;
-    if ((rc = check_cuda(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev), "SM count"))) return rc;
-  }
+  int n_sm = 0;
+  if ((rc = current_sm_count(&n_sm))) return rc;
   const int grid_p = (int)(grid_q < n_sm ? grid_q : n_sm);
   attn_bwd_dqp_kernel<D, VARLEN><<<(unsigned)grid_p, DqCfg<D>::kThreads, DqCfg<D>::kSmemBytes, stream>>>(
       tmQ, tmK, tmV, tmDO, a, (int)grid_q);

@@ -8,11 +8,14 @@
 
 namespace bd {
 
-// 4-D TMA map over a [b, N, H, D] bf16 tensor: dims (D, H, N, b), box
-// (64, 1, 128, 1), 128-byte swizzle.  Rows past N are zero-filled.
-inline bool make_qkv_tmap(CUtensorMap* m, const void* base, int batch, int N, int H, int D, int box_rows = 128) {
+// 4-D TMA map over a [b, N, H, D] bf16 tensor whose token rows hold
+// row_heads >= H heads in memory (head sharding; 0 = H): dims (D, H, N, b),
+// box (64, 1, 128, 1), 128-byte swizzle.  Rows past N are zero-filled.
+inline bool make_qkv_tmap(CUtensorMap* m, const void* base, int batch, int N, int H, int D, int box_rows = 128,
+                          int row_heads = 0) {
+  const uint64_t RH = row_heads > 0 ? (uint64_t)row_heads : (uint64_t)H;
   const uint64_t dims[4] = {(uint64_t)D, (uint64_t)H, (uint64_t)N, (uint64_t)batch};
-  const uint64_t strides[3] = {(uint64_t)D * 2, (uint64_t)H * D * 2, (uint64_t)N * H * D * 2};
+  const uint64_t strides[3] = {(uint64_t)D * 2, RH * D * 2, (uint64_t)N * RH * D * 2};
   const uint32_t box[4] = {64, 1, (uint32_t)box_rows, 1};
   return make_tmap_bf16(m, base, 4, dims, strides, box);
 }

@@ -67,6 +67,7 @@ struct FwdArgs {
   __nv_bfloat16* o;
   float* lse;
   int batch, n_q_heads, n_hg, group, N, n_kv;
+  int q_row_heads;  // heads per token row of o in memory
   Geom g;
   float scale_log2;
   int trace;
@@ -372,7 +373,7 @@ __global__ void __launch_bounds__(FwdCfg<D, NQ>::kThreads, 1)
     const int h = h0 + q;
     const bool valid = row < q1;
     const float inv_l = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* orow = a.o + (((size_t)b * a.N + row) * a.n_q_heads + h) * D;
+    __nv_bfloat16* orow = a.o + (((size_t)b * a.N + row) * a.q_row_heads + h) * D;
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       uint32_t ov[32];
@@ -404,16 +405,13 @@ int launch_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
                float* lse, const int* map, int map_stride, cudaStream_t stream) {
   using C = FwdCfg<D, NQ>;
   CUtensorMap tmQ, tmK, tmV;
-  if (!make_qkv_tmap(&tmQ, q, p.batch, g.N, p.n_q_heads, D) || !make_qkv_tmap(&tmK, k, p.batch, g.N, p.n_kv_heads, D) ||
-      !make_qkv_tmap(&tmV, v, p.batch, g.N, p.n_kv_heads, D))
+  if (!make_qkv_tmap(&tmQ, q, p.batch, g.N, p.n_q_heads, D, 128, q_row_heads(p)) ||
+      !make_qkv_tmap(&tmK, k, p.batch, g.N, p.n_kv_heads, D, 128, kv_row_heads(p)) ||
+      !make_qkv_tmap(&tmV, v, p.batch, g.N, p.n_kv_heads, D, 128, kv_row_heads(p)))
     return set_error(BD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, NQ, VARLEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::kSmemBytes);
-    if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(fwd)");
-    attr = true;
-  }
+  if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(attn_fwd_kernel<D, NQ, VARLEN>), C::kSmemBytes,
+                                "cudaFuncSetAttribute(fwd)"))
+    return rc;
   FwdArgs a;
   a.map = map;
   a.map_stride = map_stride;
@@ -421,6 +419,7 @@ int launch_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   a.lse = lse;
   a.batch = p.batch;
   a.n_q_heads = p.n_q_heads;
+  a.q_row_heads = q_row_heads(p);
   a.n_hg = p.n_q_heads / NQ;
   a.group = p.n_q_heads / p.n_kv_heads;
   a.n_kv = p.n_kv_heads;

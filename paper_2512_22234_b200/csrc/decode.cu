@@ -450,12 +450,9 @@ __global__ void select_commit_kernel(int batch, int B, const uint8_t* __restrict
 template <int NQ>
 int launch_decode(const CUtensorMap& tK, const CUtensorMap& tV, const DecArgs& a, cudaStream_t stream) {
   using C = DecCfg<NQ>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(decode)");
-    attr = true;
-  }
+  if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(decode_attn_kernel<NQ>), C::kSmem,
+                                "cudaFuncSetAttribute(decode)"))
+    return rc;
   dim3 grid(a.n_splits, a.Hkv * a.n_parts, a.batch);
   decode_attn_kernel<NQ><<<grid, kDThreads, C::kSmem, stream>>>(tK, tV, a);
   note_launches(1);

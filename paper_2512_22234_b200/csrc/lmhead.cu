@@ -348,13 +348,9 @@ bool tmap2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, ui
 
 template <int EPI, bool A_MN, bool B_MN>
 int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, GemmParams p, const Plan& pl, cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm2sm_kernel<EPI, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kSmemG);
-    if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(gemm2sm)");
-    attr = true;
-  }
+  if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(gemm2sm_kernel<EPI, A_MN, B_MN>), kSmemG,
+                                "cudaFuncSetAttribute(gemm2sm)"))
+    return rc;
   p.n_tiles = pl.n_tiles;
   p.n_chunks = pl.n_chunks;
   p.tiles_per_chunk = pl.tpc;

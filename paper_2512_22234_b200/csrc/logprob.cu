@@ -439,12 +439,9 @@ extern "C" int bd_logprob(int64_t n_rows, int32_t vocab, const void* logits, int
   if (fusable) {
     // one HBM read + one HBM write: the row stays in the cluster's shared memory
     const int smem = vocab / kCl * 2;
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(logprob_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(logprob_fused)");
-      attr = true;
-    }
+    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(logprob_fused_kernel), 200 * 1024,
+                                  "cudaFuncSetAttribute(logprob_fused)"))
+      return rc;
     if (smem > 200 * 1024) return set_error(BD_ERR_UNSUPPORTED, "vocab too large for the fused path");
     logprob_fused_kernel<<<(unsigned)(n_rows * kCl), kFusedThreads, smem, stream>>>(
         vocab, reinterpret_cast<const __nv_bfloat16*>(logits), row_stride, targets, logp, lse, dlogp,

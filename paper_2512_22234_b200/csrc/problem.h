@@ -30,6 +30,10 @@ inline int validate_problem(const bd_problem* p) {
   const int64_t NT = (L + kTileRows - 1) / kTileRows + S * ((Lx + kTileRows - 1) / kTileRows);
   if (NT > kMaxTiles) return set_error(BD_ERR_UNSUPPORTED, "sequence too long for the tile map (%lld tiles)",
                                        (long long)NT);
+  if (p->q_row_heads < 0 || p->kv_row_heads < 0 || (p->q_row_heads && p->q_row_heads < p->n_q_heads) ||
+      (p->kv_row_heads && p->kv_row_heads < p->n_kv_heads))
+    return set_error(BD_ERR_INVALID_ARG, "row heads (%d, %d) below (n_q_heads, n_kv_heads) = (%d, %d)", p->q_row_heads,
+                     p->kv_row_heads, p->n_q_heads, p->n_kv_heads);
   if ((p->seq_prompt_len == nullptr) != (p->seq_response_len == nullptr))
     return set_error(BD_ERR_INVALID_ARG, "seq_prompt_len and seq_response_len must both be set or both null");
   if (p->seq_prompt_len) {
@@ -73,6 +77,10 @@ inline SeqLens seq_lens_of(const bd_problem& p) {
   }
   return s;
 }
+
+// Heads per token row in memory (head sharding; 0 = dense).
+inline int q_row_heads(const bd_problem& p) { return p.q_row_heads ? p.q_row_heads : p.n_q_heads; }
+inline int kv_row_heads(const bd_problem& p) { return p.kv_row_heads ? p.kv_row_heads : p.n_kv_heads; }
 
 inline float scale_of(const bd_problem& p) {
   return p.softmax_scale > 0.f ? p.softmax_scale : 1.0f / std::sqrt((float)p.head_dim);

@@ -218,11 +218,14 @@ struct MapView {
   __host__ __device__ int* bwd_order() const { return fwd_order() + NT; }
 };
 
-// Upper bound on entries: a q-tile lists at most T0 x0 tiles and 2 tiles of its own copy
-// (its own block spans at most two xt tiles when B <= 128; in general
-// ceil(B/128)+1).
+// Upper bound on entries: a q-tile lists at most T0 x0 tiles and xt_max tiles
+// of its own copy.  Its rows' own-copy intervals union to [blockstart(p0),
+// blockend(p0 + 127)), at most 126 + 2B keys at any offset -- blocks need not
+// be tile-aligned (B not dividing 128, or xb % B != 0 in response-only mode) --
+// so at most ceil((126 + 2B) / 128) + 1 tiles.  The device builder also uses
+// capacity / NT as the per-q-tile stride of its staged entries.
 __host__ __device__ inline int map_capacity(const Geom& g) {
-  const int xt_max = (g.B + kTileRows - 1) / kTileRows + 1;
+  const int xt_max = (2 * g.B + 126 + kTileRows - 1) / kTileRows + 1;
   return g.NT * (g.T0 + (xt_max < g.T1 ? xt_max : g.T1));
 }
 __host__ __device__ inline long long map_words(const Geom& g) {

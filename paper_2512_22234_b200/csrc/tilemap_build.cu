@@ -320,11 +320,9 @@ int build_map_device(const Geom& g, int* ws, cudaStream_t stream) {
   int stage = 0;
   const size_t smem = build_smem(g, stage);
   if (g.NT > kMaxTiles) return set_error(BD_ERR_UNSUPPORTED, "too many tiles (%d > %d)", g.NT, kMaxTiles);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(build_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_done = true;
-  }
+  if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(build_map_kernel), 227 * 1024,
+                                "cudaFuncSetAttribute(build_map_kernel)"))
+    return rc;
   build_map_kernel<<<1, kBuildThreads, smem, stream>>>(g, ws, stage);
   note_launches(1);
   return check_cuda(cudaGetLastError(), "build_map_kernel launch");
@@ -334,11 +332,9 @@ int build_map_device_varlen(const Geom& gmax, const SeqLens& lens, int* ws, long
   int stage = 0;
   const size_t smem = build_smem(gmax, stage);
   if (gmax.NT > kMaxTiles) return set_error(BD_ERR_UNSUPPORTED, "too many tiles (%d > %d)", gmax.NT, kMaxTiles);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(build_map_varlen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_done = true;
-  }
+  if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(build_map_varlen_kernel), 227 * 1024,
+                                "cudaFuncSetAttribute(build_map_varlen_kernel)"))
+    return rc;
   build_map_varlen_kernel<<<lens.n, kBuildThreads, smem, stream>>>(lens, ws, stride, stage);
   note_launches(1);
   return check_cuda(cudaGetLastError(), "build_map_varlen_kernel launch");
@@ -431,6 +427,44 @@ extern "C" int bd_tilemap_selfcheck(const bd_problem* prob, int64_t* mismatches)
     }
   }
   *mismatches = bad;
+  return BD_OK;
+}
+
+// Element-level mask the kernels evaluate (host, tests): for rows
+// [row0, row0 + n_rows) of sequence `seq`, every packed key of that sequence,
+// bit 0 = key inside the row's interval (row_interval: forward and dQ
+// kernels), bit 1 = row inside the key's interval (key_interval: dK/dV
+// kernel).  Tests compare both bits with the oracle's dense mask.
+extern "C" int bd_mask_dump(const bd_problem* prob, int32_t seq, int64_t row0, int64_t n_rows, uint8_t* host_out,
+                            size_t cap, int64_t* n_keys) {
+  using namespace bd;
+  int rc = validate_problem(prob);
+  if (rc) return rc;
+  if (seq < 0 || seq >= prob->batch) return set_error(BD_ERR_INVALID_ARG, "sequence %d out of range", seq);
+  Geom g = geom_of(*prob);
+  if (is_varlen(*prob)) {
+    const int P = prob->seq_prompt_len[seq], R = prob->seq_response_len[seq];
+    g = make_geom(P + R, prob->repeat_prompt ? 0 : P, prob->block_size, prob->n_copies);
+  }
+  if (n_keys) *n_keys = g.N;
+  if (row0 < 0 || n_rows < 0 || row0 + n_rows > g.N) return set_error(BD_ERR_INVALID_ARG, "row range outside [0, %d)", g.N);
+  if (cap < (size_t)n_rows * g.N) return set_error(BD_ERR_WORKSPACE, "capacity %zu < %lld", cap, (long long)n_rows * g.N);
+  if (!host_out && n_rows) return set_error(BD_ERR_INVALID_ARG, "host_out is null");
+  for (int64_t i = 0; i < n_rows; ++i) {
+    const int r = (int)(row0 + i);
+    const int qs = seg_of_row(g, r);
+    int lo[64], hi[64];
+    const int nseg = 1 + g.S;
+    if (nseg > 64) return set_error(BD_ERR_UNSUPPORTED, "too many copies for the dump");
+    for (int s = 0; s < nseg; ++s) row_interval(g, qs, r, s, lo[s], hi[s]);
+    uint8_t* o = host_out + i * g.N;
+    for (int k = 0; k < g.N; ++k) {
+      const int ks = seg_of_row(g, k);
+      int qa, qb;
+      key_interval(g, ks, k, qs, qa, qb);
+      o[k] = (uint8_t)((k >= lo[ks] && k < hi[ks]) | ((r >= qa && r < qb) << 1));
+    }
+  }
   return BD_OK;
 }
 

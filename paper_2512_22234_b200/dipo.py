@@ -14,21 +14,17 @@ Eq. 8 with the stop-gradient behaviour policy of Eq. 7
 import torch
 import torch.distributed as dist
 
-from . import ops
+from . import ops, shard
 
 
 def shard_range(n_units: int, world: int, rank: int):
     """Contiguous sharding of n_units sequences: rank r gets [r n/W, (r+1) n/W)."""
-    return (rank * n_units) // world, ((rank + 1) * n_units) // world
+    return shard.shard_range(n_units, world, rank)
 
 
-def groups_straddle(n_seq: int, group_size: int, world: int) -> bool:
-    """True if some GRPO group is split across ranks by shard_range."""
-    for r in range(world):
-        a, b = shard_range(n_seq, world, r)
-        if a % group_size or (b % group_size and b != n_seq):
-            return True
-    return False
+def groups_straddle(n_seq: int, group_size: int, world: int, n_kv: int = 1) -> bool:
+    """True if some GRPO group is split across ranks (see shard.groups_straddle)."""
+    return shard.groups_straddle(n_seq, group_size, world, n_kv)
 
 
 def _dist_on(pg):

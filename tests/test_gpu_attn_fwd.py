@@ -26,6 +26,17 @@ CASES = [
     ("copies3_resp_only_ragged", AttnConfig("t2", 1, 2, 1, 128, 40, 200, 8, repeat_prompt=0, n_copies=3)),
     ("copies4_d64_B1", AttnConfig("t3", 1, 2, 2, 64, 0, 136, 1, n_copies=4)),
     ("copies2_B128", AttnConfig("t4", 1, 2, 1, 128, 128, 256, 128, n_copies=2)),
+    # block sizes that do not divide 128 (a block straddles a tile edge: PARTIAL
+    # tiles whose block boundaries are not tile-aligned) and response-only mode
+    # with P % B != 0 (the first noisy row starts mid-block)
+    ("B12_gqa2", AttnConfig("n1", 1, 4, 2, 128, 36, 264, 12)),
+    ("B48_resp_only_P50", AttnConfig("n2", 1, 4, 2, 128, 50, 334, 48, repeat_prompt=0)),
+    ("B96_d64", AttnConfig("n3", 1, 2, 1, 64, 96, 288, 96)),
+    ("B200_resp_only_P130", AttnConfig("n4", 1, 2, 2, 128, 130, 470, 200, repeat_prompt=0)),
+    ("resp_only_P42_B8", AttnConfig("n5", 2, 4, 2, 128, 42, 214, 8, repeat_prompt=0)),
+    ("resp_only_P33_B3_odd_group", AttnConfig("n6", 1, 3, 1, 128, 33, 267, 3, repeat_prompt=0)),
+    ("copies3_B12", AttnConfig("n7", 1, 4, 2, 128, 36, 264, 12, n_copies=3)),
+    ("copies2_resp_only_B12_P42", AttnConfig("n8", 1, 2, 1, 128, 42, 258, 12, repeat_prompt=0, n_copies=2)),
 ]
 
 

@@ -36,15 +36,19 @@ def _meaningful(img, NT, cap):
     (32, 64, 4, 1, 1),        # tiny, L < 128
     (7, 121, 128, 1, 1),      # B = 128, P % B != 0
     (4096, 28672, 4, 1, 1),   # L = 32k (NT = 512)
+    # blocks not aligned to tiles: B not dividing 128, xb % B != 0 (a q-tile's
+    # own-copy tiles exceeded the staged per-tile stride before the fix)
+    (50, 334, 48, 0, 1), (36, 264, 12, 1, 3), (100, 284, 96, 0, 1), (130, 470, 200, 0, 1),
+    (42, 214, 8, 0, 2), (5, 355, 5, 1, 1),
 ])
 def test_device_map_equals_host_image(cuda_ok, P, R, B, rp, S):
     prob = bd.Problem(1, P, R, B, 1, 1, 64, repeat_prompt=rp, n_copies=S)
     host = ops.tilemap_host_image(prob)
     N = bd.packed_len(prob)
     q = torch.zeros((1, N, 1, 64), dtype=torch.bfloat16, device="cuda")
-    ops.attn_fwd(prob, q, q, q)
+    ws = torch.full((bd.workspace_bytes(prob, False),), 0xFF, dtype=torch.uint8, device="cuda")
+    ops.attn_fwd(prob, q, q, q, ws=ws)
     torch.cuda.synchronize()
-    ws = ops._ws_cache[torch.device("cuda").index if torch.device("cuda").index is not None else 0]
     dev = ws[:4 * len(host)].view(torch.int32).cpu().tolist()
     NT, T0 = host[4], host[5]
     cap = (len(host) - HDR - 2 * (NT + 1) - 2 * NT) // 2

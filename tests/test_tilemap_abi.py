@@ -63,7 +63,12 @@ def test_packed_len_and_workspace():
 def _cases():
     for P, R, B, rp in [(32, 64, 4, 1), (0, 256, 4, 1), (0, 384, 128, 1), (64, 320, 8, 1), (40, 160, 8, 1),
                         (40, 160, 8, 0), (100, 300, 4, 0), (0, 512, 256, 1), (0, 512, 1, 1), (24, 0, 1, 0),
-                        (130, 126, 2, 1), (7, 121, 128, 1), (300, 600, 300, 1), (5, 5, 10, 0)]:
+                        (130, 126, 2, 1), (7, 121, 128, 1), (300, 600, 300, 1), (5, 5, 10, 0),
+                        # block sizes that do not divide 128 (blocks straddle tile edges) and
+                        # response-only mode with P % B != 0 (first noisy row mid-block)
+                        (36, 264, 12, 1), (42, 258, 12, 0), (42, 214, 8, 0), (48, 336, 48, 1),
+                        (50, 334, 48, 0), (96, 288, 96, 1), (100, 284, 96, 0), (0, 600, 200, 1),
+                        (130, 470, 200, 0), (33, 267, 3, 0)]:
         yield P, R, B, rp
 
 
@@ -138,3 +143,26 @@ def test_varlen_validation_and_workspace():
         assert L.bd_packed_len(ctypes.byref(p.c())) == -1
     half = bd.Problem(3, 64, 320, 4, 4, 2, 128, seq_prompt_lens=(64, 32, 0))
     assert L.bd_packed_len(ctypes.byref(half.c())) == -1
+
+
+def test_row_length_within_capacity_stride_random():
+    """Every q-tile's entry count fits the per-q-tile stride (capacity / NT)
+    that the device builder stages entries with -- including block sizes that
+    do not divide 128 and xb % B != 0 (a regression: B = 48, P = 50,
+    response-only overflowed the stride and corrupted the device map)."""
+    import random
+    rng = random.Random(7)
+    cases = [(50, 334, 48, 0, 1), (100, 284, 96, 0, 1), (130, 470, 200, 0, 1), (36, 264, 12, 1, 3)]
+    for _ in range(300):
+        B = rng.choice([1, 2, 3, 4, 5, 7, 8, 12, 16, 24, 32, 48, 64, 96, 100, 128, 200, 256, 300])
+        K = rng.randint(1, max(1, 1500 // B))
+        L = K * B
+        P = rng.randint(0, L)
+        cases.append((P, L - P, B, rng.randint(0, 1), rng.choice([1, 1, 2, 3])))
+    for P, R, B, rp, S in cases:
+        if P + R - (0 if rp else P) <= 0:
+            continue
+        img = bd.ops.tilemap_host_image(bd.Problem(1, P, R, B, 1, 1, 64, repeat_prompt=rp, n_copies=S))
+        NT, maxrow = img[4], img[7]
+        cap = (len(img) - 16 - 2 * (NT + 1) - 2 * NT) // 2
+        assert maxrow <= cap // NT, (P, R, B, rp, S, maxrow, cap // NT)
