@@ -138,9 +138,9 @@ __device__ __forceinline__ void softmax_tile(uint32_t tS, uint32_t tO, int lo, i
     const float2 x = ffma2(make_float2(s[2 * c], s[2 * c + 1]), sl2v, nm);
     float2 p;
     if (BD_FWD_POLY_MOD > 0 && (c % BD_FWD_POLY_MOD) == BD_FWD_POLY_MOD - 1) {
-      p = ex2_poly2(x);
+      p = ex2_poly2(x);  // exactly +0 for a masked (-inf) score, like the MUFU's ex2
     } else {
-      p.x = ex2_approx(x.x);
+      p.x = ex2_approx(x.x);  // ex2.approx(-inf) = +0
       p.y = ex2_approx(x.y);
     }
     acc[c & 3] = fadd2(acc[c & 3], p);

@@ -241,9 +241,13 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // x = n + r with n = rint(x) (1.5*2^23 magic), r in [-0.5, 0.5];
 // 2^r ~ 1 + r(c1 + r(c2 + r c3)) (relative-error fit, max 1.0e-4 -- far below
 // bf16's 2^-9 rounding of P); 2^n added to the exponent bits.  x is clamped
-// at -126 so the result stays >= 2^-126 (never wraps); x <= 127.
+// at -127: n >= -127 and, for n = -127, r >= 0 and p >= 1, so the exponent
+// field never wraps; x <= -127 (a masked -inf score included) gives r = 0,
+// p = 1.0 and the bits of +0.0 -- a masked key gets exactly zero weight, as
+// with the MUFU's ex2.approx.ftz (arguments in (-127, -126) land on
+// denormal-range values ~2^-127 instead of flushing; harmless).  x <= 127.
 __device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -126.f);
+  x = fmaxf(x, -127.f);
   const float t = x + 12582912.f;
   const float r = x - (t - 12582912.f);
   float p = fmaf(0.05500893f, r, 0.24221098f);
@@ -287,8 +291,8 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
 // 2^x for a pair on the FMA pipe, packed (same fit as ex2_poly): ~5 issue
 // slots per element against the MUFU's 8-clock-per-warp ex2.
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
   const float2 magic = make_float2(12582912.f, 12582912.f);
   const float2 t = fadd2(x, magic);
   const float2 tm = fadd2(t, make_float2(-12582912.f, -12582912.f));

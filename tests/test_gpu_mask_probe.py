@@ -152,7 +152,7 @@ def test_mask_probe_grid(cuda_ok, P, R, B, rp, S):
 @pytest.mark.parametrize("G,d", [(1, 128), (2, 64), (3, 64)])
 def test_mask_probe_other_instantiations(cuda_ok, G, d):
     """NQ = 1 forward (odd group) and d = 64 kernels."""
-    _probe(42, 214, 12, 0, 1, Hkv=4, G=G, d=d)
+    _probe(42, 258, 12, 0, 1, Hkv=4, G=G, d=d)
 
 
 def test_mask_probe_sdar_1_7b(cuda_ok):
