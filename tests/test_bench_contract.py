@@ -54,3 +54,21 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "TFLOP/s"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["config"]["workload"] == "sdar_1_7b"
+
+
+def test_job_accounting_over_ranks():
+    """Strong-scaling jobs keep the whole job's useful FLOPs fixed as W grows
+    (units partition the job); BJ configs[4] totals 4,990 TFLOP fwd+bwd
+    (SURVEY §8(d)); weak jobs grow linearly."""
+    sys.path.insert(0, ROOT)
+    import bench
+    for name in ("rl8", "fig6", "sdar_8b_strong"):
+        job = bench.JOBS[name]
+        tot = [sum(bench.job_flops(job, w)) for w in (1, 2, 4, 8)]
+        assert max(tot) - min(tot) < 1e-6 * tot[0], (name, tot)
+    assert abs(sum(bench.job_flops(bench.JOBS["rl8"], 8)) / 1e12 - 4990) < 1
+    w1 = sum(bench.job_flops(bench.JOBS["sdar_8b"], 1))
+    assert abs(sum(bench.job_flops(bench.JOBS["sdar_8b"], 8)) - 8 * w1) < 1e-6 * w1
+    # fig6 at W = 8: every rank runs half of one sequence's heads
+    f = [bench.rank_flops(bench.JOBS["fig6"], 8, r)[0] for r in range(8)]
+    assert max(f) == min(f)
