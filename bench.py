@@ -539,39 +539,41 @@ def run_e2e(step, args, world, flops_step):
     copied = [torch.cuda.Event(), torch.cuda.Event()]
     computed = [torch.cuda.Event(), torch.cuda.Event()]
     drained = [torch.cuda.Event(), torch.cuda.Event()]
-    h2d = d2h = 0
     npc = len(step.pieces)
+    tally = {"h2d": 0, "d2h": 0}
 
-    def one_step():
-        nonlocal h2d, d2h
-        h2d = d2h = 0
+    def copy_in(i, sl):
+        n = step.pieces[i].n_seq
+        s_in.wait_event(computed[sl])  # the slot's previous micro-batch no longer reads its inputs
+        with torch.cuda.stream(s_in):
+            for nm in names_in:
+                src = host_in[nm][:step.piece_rows[i]] if nm == "targets" else host_in[nm][:n]
+                dst = slots[sl][nm][:step.piece_rows[i]] if nm == "targets" else slots[sl][nm][:n]
+                dst.copy_(src, non_blocking=True)
+                tally["h2d"] += src.numel() * src.element_size()
+            copied[sl].record(s_in)
+
+    def run(n_steps):
+        """n_steps steps as one stream of micro-batches: the copy-in of the
+        next micro-batch (of this step or the next) overlaps the compute of the
+        current one, whose copy-out overlaps the one after."""
         for e in computed + drained:
             e.record(main)
-        step.rewards.copy_(host_rew, non_blocking=True)
-        h2d += host_rew.numel() * 4
-        dlogp, parts = step.dipo()
-
-        def copy_in(i):
-            nonlocal h2d
-            sl = i % 2
-            n = step.pieces[i].n_seq
-            s_in.wait_event(computed[sl])  # slot's previous micro-batch no longer reads its inputs
-            with torch.cuda.stream(s_in):
-                for nm in names_in:
-                    src = host_in[nm][:step.piece_rows[i]] if nm == "targets" else host_in[nm][:n]
-                    dst = slots[sl][nm][:step.piece_rows[i]] if nm == "targets" else slots[sl][nm][:n]
-                    dst.copy_(src, non_blocking=True)
-                    h2d += src.numel() * src.element_size()
-                copied[sl].record(s_in)
-
-        copy_in(0)
+        order = [(s, i) for s in range(n_steps) for i in range(npc)]
+        copy_in(0, 0)
+        dlogp = parts = None
         r0 = 0
-        for i in range(npc):
-            sl = i % 2
-            if i + 1 < npc:
-                copy_in(i + 1)
+        for idx, (s, i) in enumerate(order):
+            sl = idx % 2
+            if i == 0:
+                step.rewards.copy_(host_rew, non_blocking=True)
+                tally["h2d"] += host_rew.numel() * 4
+                dlogp, parts = step.dipo()
+                r0 = 0
+            if idx + 1 < len(order):
+                copy_in(order[idx + 1][1], 1 - sl)
             main.wait_event(copied[sl])
-            main.wait_event(drained[sl])  # slot's previous outputs copied out
+            main.wait_event(drained[sl])  # the slot's previous outputs are copied out
             logp = step.run_piece(i, dlogp, r0, bufs=slots[sl])
             computed[sl].record(main)
             s_out.wait_event(computed[sl])
@@ -579,33 +581,35 @@ def run_e2e(step, args, world, flops_step):
             with torch.cuda.stream(s_out):
                 for nm in names_out:
                     host_out[nm][:n].copy_(slots[sl][nm][:n], non_blocking=True)
-                    d2h += host_out[nm][:n].numel() * 2
+                    tally["d2h"] += host_out[nm][:n].numel() * 2
                 if logp is not None:
                     host_logp[:logp.numel()].copy_(logp, non_blocking=True)
-                    d2h += logp.numel() * 4
+                    tally["d2h"] += logp.numel() * 4
+                if i == npc - 1:
+                    host_loss.copy_(parts, non_blocking=True)
+                    tally["d2h"] += 24
                 drained[sl].record(s_out)
             r0 += step.piece_rows[i]
         main.wait_stream(s_out)
-        host_loss.copy_(parts, non_blocking=True)
-        d2h += 24
 
-    one_step()  # warm path
+    run(1)  # warm path
     barrier(world)
     n_steps = max(2, min(args.steps, 6))
+    tally["h2d"] = tally["d2h"] = 0
     es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     es.record()
-    for _ in range(n_steps):
-        one_step()
+    run(n_steps)
     ee.record()
     barrier(world)
+    h2d, d2h = tally["h2d"] // n_steps, tally["d2h"] // n_steps
     e2e_ms = max_over_ranks(es.elapsed_time(ee) / n_steps, world)
     return {"value": round(flops_step / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
             "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "steps": n_steps,
             "inputs": "q, k, v, dO, targets of every micro-batch and the rewards H2D from pinned host; dQ, dK, dV "
                       "and logp of every micro-batch and the DiPO loss partials D2H (H2D / D2H streams, two "
-                      "device slots, overlapped with compute); the logits are the caller's LM-head output and stay "
-                      "device-resident"}
+                      "device slots; micro-batches of consecutive steps form one pipeline, copies overlapped with "
+                      "compute); the logits are the caller's LM-head output and stay device-resident"}
 
 
 def _timeit(fn, reps=5):
