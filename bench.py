@@ -646,9 +646,14 @@ def bench_configs(peaks, names=None):
         q, k, v, do = attn_inputs(cfg, device="cuda")
         o, lse = bd.attn_fwd(prob, q, k, v)
         dq, dk, dv = bd.attn_bwd(prob, q, k, v, o, lse, do)
+        # enough repetitions for >= ~1.5 s of timed work, so nvidia-smi (200 ms)
+        # samples the clocks of every config
+        t0 = _timeit(lambda: (bd.attn_fwd(prob, q, k, v, o, lse), bd.attn_bwd(prob, q, k, v, o, lse, do, dq, dk, dv)),
+                     reps=1)
+        reps = int(min(200, max(5, 750.0 / max(t0, 1e-3))))
         with ClockSampler(torch.cuda.current_device()) as clk:
-            tf = _timeit(lambda: bd.attn_fwd(prob, q, k, v, o, lse))
-            tb = _timeit(lambda: bd.attn_bwd(prob, q, k, v, o, lse, do, dq, dk, dv))
+            tf = _timeit(lambda: bd.attn_fwd(prob, q, k, v, o, lse), reps)
+            tb = _timeit(lambda: bd.attn_bwd(prob, q, k, v, o, lse, do, dq, dk, dv), reps)
         f, fb = useful_flops(cfg)
         if cfg.resp_lens is None:
             st = ops.tilemap_stats(prob)
@@ -664,7 +669,7 @@ def bench_configs(peaks, names=None):
         out[name] = {"batch": cfg.batch, "heads": f"{cfg.n_q_heads}/{cfg.n_kv_heads}", "head_dim": cfg.head_dim,
                      "prompt_len": cfg.prompt_len, "response_len": cfg.response_len, "block_size": cfg.block_size,
                      "n_copies": cfg.n_copies, "varlen": cfg.resp_lens is not None,
-                     "fwd_ms": round(tf, 3), "bwd_ms": round(tb, 3),
+                     "fwd_ms": round(tf, 3), "bwd_ms": round(tb, 3), "reps": reps,
                      "fwd_tflops": round(f / tf / 1e9, 1), "bwd_tflops": round(fb / tb / 1e9, 1),
                      "fwd_bwd_tflops": round((f + fb) / (tf + tb) / 1e9, 1),
                      "fwd_bwd_frac_sustained": round((f + fb) / (tf + tb) / 1e9 / peak, 4),

@@ -1,7 +1,8 @@
 """Tiny end-to-end run of every ABI entry point, for compute-sanitizer
 (memcheck / racecheck / synccheck / initcheck): attention fwd + bwd (uniform,
-varlen, trace replay), fused and two-pass logprob, DiPO, LM head fwd + bwd,
-decode attention + select.  Exits 0 when every call returned BD_OK."""
+varlen, trace replay, d = 64, blocks not aligned to tiles, head-sharded
+strided slices), fused and two-pass logprob, DiPO, LM head fwd + bwd, decode
+attention + select.  Exits 0 when every call returned BD_OK."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -16,6 +17,22 @@ for cfg in (base, base.with_(resp_lens=(160,), batch=1), base.with_(n_copies=2),
     q, k, v, do = [x.cuda() for x in attn_inputs(cfg)]
     o, lse = bd.attn_fwd(prob, q, k, v)
     bd.attn_bwd(prob, q, k, v, o, lse, do)
+# block sizes that straddle tile edges / xb % B != 0 (response-only), and a
+# head-sharded problem on strided head slices of full-width tensors
+for cfg in (base.with_(prompt_len=50, response_len=334, block_size=48, repeat_prompt=0),
+            base.with_(prompt_len=36, response_len=264, block_size=12, n_copies=2)):
+    prob = bd.Problem.from_cfg(cfg)
+    q, k, v, do = [x.cuda() for x in attn_inputs(cfg)]
+    o, lse = bd.attn_fwd(prob, q, k, v)
+    bd.attn_bwd(prob, q, k, v, o, lse, do)
+cfg = base.with_(n_q_heads=8, n_kv_heads=4)
+full = bd.Problem.from_cfg(cfg)
+q, k, v, do = [x.cuda() for x in attn_inputs(cfg)]
+sh = full.head_shard(1, 2)
+qs, dos = sh.head_slice_q(q), sh.head_slice_q(do)
+ks, vs = sh.head_slice_kv(k), sh.head_slice_kv(v)
+o, lse = bd.attn_fwd(sh, qs, ks, vs)
+bd.attn_bwd(sh, qs, ks, vs, o, lse, dos)
 z, t = logits_inputs(64, 1024, seed=1)
 z, t = z.cuda(), t.cuda()
 logp, lz = ops.logprob(z, t)

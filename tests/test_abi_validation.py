@@ -78,3 +78,19 @@ def test_dipo_validation_names():
                        (UNSUPPORTED, b"BD_ERR_UNSUPPORTED"), (ALIGN, b"BD_ERR_ALIGNMENT"), (6, b"BD_ERR_CUDA")):
         assert lib.bd_error_string(code) == name
     assert lib.bd_error_string(99) == b"BD_ERR_UNKNOWN"
+
+
+def test_binding_rejects_host_tensors():
+    """The binding never passes host pointers to the device path (no CPU fallback)."""
+    import pytest
+    import torch
+    import paper_2512_22234_b200 as bd
+    from paper_2512_22234_b200._lib import BdError
+    prob = bd.Problem(1, 32, 64, 4, 2, 2, 64)
+    q = torch.zeros((1, prob.ntot, 2, 64), dtype=torch.bfloat16)
+    with pytest.raises(BdError, match="CUDA"):
+        bd.attn_fwd(prob, q, q, q)
+    with pytest.raises(BdError, match="CUDA"):
+        bd.ops.logprob(torch.zeros((2, 8), dtype=torch.bfloat16), torch.zeros(2, dtype=torch.int32))
+    with pytest.raises(BdError, match="outside"):
+        prob.head_shard(1, 2)
