@@ -29,7 +29,7 @@ def _setup():
 def test_attention_argument_checks(cuda_ok):
     cfg, prob, q, k, v, do = _setup()
     n0 = ops.launch_count()
-    with pytest.raises(BdError, match="bf16"):
+    with pytest.raises(BdError, match="bfloat16"):
         bd.attn_fwd(prob, q.float(), k, v)
     with pytest.raises(BdError, match="shape"):
         bd.attn_fwd(prob, q[:, :-1], k[:, :-1], v[:, :-1])
@@ -50,7 +50,7 @@ def test_attention_argument_checks(cuda_ok):
 def test_logprob_argument_checks(cuda_ok):
     z, t = logits_inputs(8, 1024, device="cuda")
     with pytest.raises(BdError, match="bf16"):
-        ops.logprob(z.float(), t)
+        ops.logprob(z.float(), t)  # _check_logits says "bf16"
     with pytest.raises(BdError, match="int32"):
         ops.logprob(z, t.long())
     with pytest.raises(BdError, match="shape"):
