@@ -78,27 +78,48 @@ def test_lmhead_bwd(cuda_ok, n, C, V, chunk):
 
 def test_lmhead_fullsize_sampled(cuda_ok):
     """SDAR-8B LM-head shape (131,072 rows x 4,096 x 151,936) in the bench launch
-    configuration; logp / LSE of 12 seeded rows and dh of 4 rows vs the oracle
-    row by row (each row is independent of the others)."""
+    configuration; logp / LSE of 14 seeded rows and dh of 4 rows vs
+    oracle.lmhead row by row (each row is independent of the others); dW over
+    all rows satisfies sum_v dW_v = 0 (every row of dz sums to zero)."""
     n, C, V = LMHEAD_SHAPES["sdar_8b"]
     h, W, t, w = lmhead_inputs(n, C, V, device="cuda", seed=11)
     ops = _ops()
     logp, lse = ops.lmhead_logprob(h, W, t)
     torch.cuda.synchronize()
     rows = torch.randint(0, n, (12,), generator=torch.Generator().manual_seed(5)).tolist() + [0, n - 1]
-    Wd = W.double().cpu().numpy()
+    Wc = W.cpu()
     hs, ts = h[rows].cpu(), t[rows].cpu().long()
-    z = hs.double().numpy() @ Wd.T
-    from oracle import logprob as olp
-    lp_ref, lse_ref = olp.logprob(z, ts.numpy())
+    lp_ref, lse_ref = olm.lmhead_logprob(hs, Wc, ts.numpy())
     m = metrics(t2np(logp[rows]), lp_ref)
     assert m["finite"] and m["max_abs"] <= LOGP_MAX_ABS, m
     assert metrics(t2np(lse[rows]), lse_ref)["max_abs"] <= LOGP_MAX_ABS
-    # backward: dh of sampled rows (dW needs every row; covered at small sizes)
     dh, dW = ops.lmhead_logprob_bwd(h, W, t, lse, w, chunk_rows=16384)
     torch.cuda.synchronize()
     sub = rows[:4]
-    dz = olp.logprob_grad(z[:4], ts[:4].numpy(), w[sub].double().cpu().numpy())
-    m = metrics(t2np(dh[sub]), dz @ Wd)
+    dh_ref, _ = olm.lmhead_logprob_grad(hs[:4], Wc, ts[:4].numpy(), w[sub].double().cpu().numpy())
+    m = metrics(t2np(dh[sub]), dh_ref)
     assert m["finite"] and m["rel_l2"] <= DZ_REL_L2, m
     assert torch.isfinite(dW).all()
+    col = dW.double().sum(0)
+    assert col.abs().max().item() <= 1e-3 * dW.double().abs().sum(0).max().item()
+
+
+def test_lmhead_full_vocab_and_hidden(cuda_ok):
+    """Full Qwen3 / SDAR-8B vocabulary and hidden size (V 151,936, C 4,096) with
+    64 rows processed in four chunks: dh and the whole dW [V, C] element by
+    element vs oracle.lmhead (every N tile, K chunk and row chunk of the four
+    GEMMs), logp / LSE of every row."""
+    n, C, V = 64, 4096, 151936
+    h, W, t, w = lmhead_inputs(n, C, V, seed=17)
+    ops = _ops()
+    hc, Wc, tc, wc = h.cuda(), W.cuda(), t.cuda(), w.cuda()
+    logp, lse = ops.lmhead_logprob(hc, Wc, tc)
+    dh, dW = ops.lmhead_logprob_bwd(hc, Wc, tc, lse, wc, chunk_rows=16)
+    torch.cuda.synchronize()
+    lp_ref, lse_ref = olm.lmhead_logprob(h, W, t.long().numpy())
+    assert metrics(t2np(logp), lp_ref)["max_abs"] <= LOGP_MAX_ABS
+    assert metrics(t2np(lse), lse_ref)["max_abs"] <= LOGP_MAX_ABS
+    dh_ref, dW_ref = olm.lmhead_logprob_grad(h, W, t.long().numpy(), w.double().numpy())
+    for name, got, ref in (("dh", dh, dh_ref), ("dW", dW, dW_ref)):
+        m = metrics(t2np(got), ref)
+        assert m["finite"] and m["rel_l2"] <= DZ_REL_L2, (name, m)
