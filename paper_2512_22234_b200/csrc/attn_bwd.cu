@@ -242,9 +242,9 @@ struct DkdvCfg {
   static constexpr int kOffVec = kOffRing + kSlots * kTileBytes;
   static constexpr int kVecBytes = 2 * 128 * 4;
   static constexpr int kOffBar = kOffVec + 2 * kVecBytes;
-  // kv_full, slot_full[S], slot_empty[S], vec_full[2], vec_empty[2], s_full, dp_full, p1_done, pt_done,
-  // acc_done, pt_half
-  static constexpr int kNumBars = 1 + 2 * kSlots + 4 + 6;
+  // kv_full, slot_full[S], slot_empty[S], vec_full[2], vec_empty[2], s_full, dp_full, p1_done,
+  // pt_done[4], acc_done, pt_half[4] (per warpgroup)
+  static constexpr int kNumBars = 1 + 2 * kSlots + 4 + 3 + 2 * kWGs + 1;
   static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16;
   static_assert(kSmemBytes <= 232448, "dkdv smem budget");
 };
@@ -269,9 +269,13 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
   uint64_t* s_full = vec_empty + 2;
   uint64_t* dp_full = s_full + 1;
   uint64_t* p1_done = dp_full + 1;  // S^T(i) read
-  uint64_t* pt_done = p1_done + 1;  // dP^T(i) read, P^T(i) written over it
-  uint64_t* acc_done = pt_done + 1;
-  uint64_t* pt_half = acc_done + 1;  // first 16 q columns of every warpgroup: P^T, dS^T written
+  // per warpgroup w: its 32 q columns' P^T(i), dS^T(i) written -- first 16
+  // (pt_half[w]) / all (pt_done[w]); the dV / dK k-steps 2w and 2w+1 read
+  // exactly those columns, so each issues as soon as its own warpgroup is
+  // done instead of waiting for the slowest of the 16 warps
+  uint64_t* pt_done = p1_done + 1;  // [4]
+  uint64_t* acc_done = pt_done + C::kWGs;
+  uint64_t* pt_half = acc_done + 1;  // [4]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
@@ -329,9 +333,9 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
     mbar_init(p1_done, C::kComputeWarps);
-    mbar_init(pt_done, C::kComputeWarps);
+    for (int w = 0; w < C::kWGs; ++w) mbar_init(&pt_done[w], 4);
     mbar_init(acc_done, 1);
-    mbar_init(pt_half, C::kComputeWarps);
+    for (int w = 0; w < C::kWGs; ++w) mbar_init(&pt_half[w], 4);
     fence_barrier_init();
     // K, V loads go out before the CTA-wide barrier and the TMEM allocation
     // (only this thread uses kv_full before the barrier)
@@ -435,28 +439,30 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
         // P^T / dS^T arrive in two halves (q columns 0-15 and 16-31 of every
         // warpgroup = the even and odd k-steps): the even k-steps of dV(i) and
         // dK(i) run while the compute warps finish the odd half
-        mbar_wait(pt_half, i & 1);
-        tc_fence_after();
+        // even k-steps (first 16 q columns of warpgroup w), then odd ones; the
+        // dV k-step order (0, 2, 4, 6, 1, 3, 5, 7) is unchanged
 #pragma unroll
-        for (int k = 0; k < 8; k += 2)
-          umma_ts(tbase + C::kColDV, tbase + C::kColDP + 32 * (k >> 1), umma_desc_sw128(doaddr + k * 2048, 16384, 1024),
+        for (int w = 0; w < C::kWGs; ++w) {
+          const int k = 2 * w;
+          mbar_wait(&pt_half[w], i & 1);
+          tc_fence_after();
+          umma_ts(tbase + C::kColDV, tbase + C::kColDP + 32 * w, umma_desc_sw128(doaddr + k * 2048, 16384, 1024),
                   idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
+          umma_ts(tbase + C::kColDK, tbase + C::kColDP + 32 * w + 16, umma_desc_sw128(qaddr + k * 2048, 16384, 1024),
+                  idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
+        }
 #pragma unroll
-        for (int k = 0; k < 8; k += 2)
-          umma_ts(tbase + C::kColDK, tbase + C::kColDP + 32 * (k >> 1) + 16,
-                  umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, (i > 0 || k > 0) ? 1u : 0u);
-        mbar_wait(pt_done, i & 1);
-        TRACE(1024 + 8 * (i & 127) + 1, blockIdx.x == 0);
-        tc_fence_after();
-#pragma unroll
-        for (int k = 1; k < 8; k += 2)
-          umma_ts(tbase + C::kColDV, tbase + C::kColDP + 32 * (k >> 1) + 8, umma_desc_sw128(doaddr + k * 2048, 16384, 1024),
+        for (int w = 0; w < C::kWGs; ++w) {
+          const int k = 2 * w + 1;
+          mbar_wait(&pt_done[w], i & 1);
+          if (w == 0) TRACE(1024 + 8 * (i & 127) + 1, blockIdx.x == 0);
+          tc_fence_after();
+          umma_ts(tbase + C::kColDV, tbase + C::kColDP + 32 * w + 8, umma_desc_sw128(doaddr + k * 2048, 16384, 1024),
                   idesc_kv, 1u);
+          umma_ts(tbase + C::kColDK, tbase + C::kColDP + 32 * w + 24, umma_desc_sw128(qaddr + k * 2048, 16384, 1024),
+                  idesc_kv, 1u);
+        }
         umma_commit(&slot_empty[slot_of(2 * i + 1)]);  // dO(i) consumed
-#pragma unroll
-        for (int k = 1; k < 8; k += 2)
-          umma_ts(tbase + C::kColDK, tbase + C::kColDP + 32 * (k >> 1) + 24,
-                  umma_desc_sw128(qaddr + k * 2048, 16384, 1024), idesc_kv, 1u);
         TRACE(1024 + 8 * (i & 127) + 5, blockIdx.x == 0);
         umma_commit(&slot_empty[slot_of(2 * i)]);  // Q(i) consumed
         if (has_next) {
@@ -551,7 +557,7 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(pt_half);
+            if (lane == 0) mbar_arrive(&pt_half[wg]);
           }
         }
       }
@@ -559,7 +565,7 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(pt_done);  // P^T(i) and dS^T(i) written: dV(i), dK(i) may be issued
+        mbar_arrive(&pt_done[wg]);  // this warpgroup's P^T(i), dS^T(i) written: its dV(i), dK(i) k-steps may issue
         mbar_arrive(&vec_empty[i & 1]);
       }
       TRACE(8 * (i & 127) + 4, blockIdx.x == 0 && threadIdx.x == 0);
