@@ -403,6 +403,7 @@ def run_ours(args):
             dist.destroy_process_group()
         return
     n_pieces = npc
+    rows_r0 = step.n_rows
     del step
     torch.cuda.empty_cache()
 
@@ -421,11 +422,9 @@ def run_ours(args):
     attn_ms = phase["attn_fwd"] + phase["attn_bwd"]
     peak_b, peak_s = peaks["bf16_tflops"], peaks["bf16_tflops_sustained"]
     bwd_per_launch = bwd_f / max(n_pieces, 1)
-    bwd_achieved = bwd_per_launch / (bwd_launch_ms * 1e-3) / 1e12
+    bwd_achieved = bwd_f / (phase["attn_bwd"] * 1e-3) / 1e12  # = per-launch FLOPs / mean launch time
     fwd_achieved = fwd_f / (phase["attn_fwd"] * 1e-3) / 1e12
-    lp_bytes = job_rows_rank0 = None
-    rows_r0 = sum(seq_resp_len(cfg, s) for s in range(job.n_seq(world))) // world
-    lp_bytes = rows_r0 * VOCAB_QWEN3 * 2
+    lp_bytes = rows_r0 * VOCAB_QWEN3 * 2  # rank 0's logits (its logprob phase time is rank 0's)
     traffic = load_traffic() if cfg.name == "sdar_8b" and job.mb() == 16 else {}
     roofline = {"kernel": "bd_attn_bwd (attn_bwd_dkdv_kernel + attn_bwd_dqp_kernel (persistent dQ) + bwd_pre + tile map)",
                 "bound": "tensor",
