@@ -95,6 +95,27 @@ def test_full_slices_sdar_8b(cuda_ok):
     _run("sdar_8b", ["first", "last"])
 
 
-def test_full_slice_sweep_b16(cuda_ok):
-    """Block-size sweep at B = 16 (L = 5,120): one seeded-random slice."""
-    _run("sweep_b16", ["random"])
+@pytest.mark.parametrize("name", ["sweep_b4", "sweep_b8", "sweep_b16", "sweep_b32"])
+def test_full_slice_sweep(cuda_ok, name):
+    """Block-size sweep (L = 5,120, B = 4 / 8 / 16 / 32): one seeded-random slice each."""
+    _run(name, ["random"])
+
+
+def test_full_slices_varlen(cuda_ok):
+    """sdar_8b_varlen (16 rollouts, R_i ~ U[512, 8192]): a complete slice of the
+    shortest and of a median-length sequence, against the oracle run on that
+    sequence alone (its own P_i, R_i), in the batch launch bench.py times."""
+    cfg = CONFIGS["sdar_8b_varlen"]
+    prob = bd.Problem.from_cfg(cfg)
+    q, k, v, do = attn_inputs(cfg, device="cuda")
+    o, lse = bd.attn_fwd(prob, q, k, v)
+    dq, dk, dv = bd.attn_bwd(prob, q, k, v, o, lse, do)
+    torch.cuda.synchronize()
+    order = sorted(range(cfg.batch), key=lambda i: cfg.resp_lens[i])
+    for bi, g in ((order[0], 3), (order[len(order) // 2], 6)):
+        one = cfg.with_(batch=1, response_len=cfg.resp_lens[bi], resp_lens=None)
+        n = one.ntot
+        sl = lambda t: t[bi:bi + 1, :n]  # noqa: E731
+        m = _check_slice(one, sl(q), sl(k), sl(v), sl(do), sl(o), lse[bi:bi + 1, :, :n], sl(dq), sl(dk), sl(dv), 0, g)
+        print("varlen", bi, cfg.resp_lens[bi], {key: (round(x["max_abs"], 5), round(x["rel_l2"], 6))
+                                                for key, x in m.items() if key.endswith("/all")})
