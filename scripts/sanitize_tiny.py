@@ -1,7 +1,7 @@
 """Tiny end-to-end run of every ABI entry point, for compute-sanitizer
 (memcheck / racecheck / synccheck / initcheck): attention fwd + bwd (uniform,
 varlen, trace replay, d = 64, blocks not aligned to tiles, head-sharded
-strided slices), fused and two-pass logprob, DiPO, LM head fwd + bwd, decode
+strided slices, a small SDAR-8B-like slice), fused and two-pass logprob, DiPO, LM head fwd + bwd, decode
 attention + select.  Exits 0 when every call returned BD_OK."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -25,6 +25,12 @@ for cfg in (base.with_(prompt_len=50, response_len=334, block_size=48, repeat_pr
     q, k, v, do = [x.cuda() for x in attn_inputs(cfg)]
     o, lse = bd.attn_fwd(prob, q, k, v)
     bd.attn_bwd(prob, q, k, v, o, lse, do)
+# a small SDAR-8B-like slice: one sequence, GQA 4, L = 2,048, B = 4
+cfg = base.with_(batch=1, n_q_heads=4, n_kv_heads=1, prompt_len=256, response_len=1792, block_size=4)
+prob = bd.Problem.from_cfg(cfg)
+q, k, v, do = [x.cuda() for x in attn_inputs(cfg)]
+o, lse = bd.attn_fwd(prob, q, k, v)
+bd.attn_bwd(prob, q, k, v, o, lse, do)
 cfg = base.with_(n_q_heads=8, n_kv_heads=4)
 full = bd.Problem.from_cfg(cfg)
 q, k, v, do = [x.cuda() for x in attn_inputs(cfg)]
