@@ -593,7 +593,8 @@ def run_e2e(step, args, world, flops_step):
 
     run(1)  # warm path
     barrier(world)
-    n_steps = max(4, min(args.steps, 24))  # the first copy-in (pipeline fill) is amortised over the run
+    # >= ~24 micro-batches: the first copy-in (pipeline fill) is amortised over the run
+    n_steps = max(2, min(args.steps, -(-24 // npc)))
     tally["h2d"] = tally["d2h"] = 0
     es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     es.record()
