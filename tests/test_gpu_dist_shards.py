@@ -134,3 +134,31 @@ def test_two_rank_units_bitwise_equal_one_rank(cuda_ok):
         assert float(out["loss"][1]) == NSEQ * R
     assert split_heads >= 2  # the middle sequence's kv heads are split between the ranks
     assert bool((rows_seen == 1).all())
+
+
+def test_head_shard_varlen_copies_d64_bitwise(cuda_ok):
+    """Head sharding composes with varlen batches, trace-replay copies and
+    d = 64: every kv-head slice run on its own (strided, no copies) is bitwise
+    equal to the same heads of the unsharded launch."""
+    import paper_2512_22234_b200 as bd
+    from workloads import AttnConfig, attn_inputs
+    cfg = AttnConfig("hs", 3, 8, 4, 64, 36, 264, 12, n_copies=2, resp_lens=(264, 120, 36))
+    prob = bd.Problem.from_cfg(cfg)
+    q, k, v, do = attn_inputs(cfg, device="cuda")
+    o, lse = bd.attn_fwd(prob, q, k, v)
+    dq, dk, dv = bd.attn_bwd(prob, q, k, v, o, lse, do)
+    G = 2
+    for kv0, n in ((0, 1), (1, 2), (3, 1)):
+        sh = prob.head_shard(kv0, n)
+        qs, dos = sh.head_slice_q(q), sh.head_slice_q(do)
+        ks, vs = sh.head_slice_kv(k), sh.head_slice_kv(v)
+        o2, l2 = bd.attn_fwd(sh, qs, ks, vs)
+        dq2, dk2, dv2 = bd.attn_bwd(sh, qs, ks, vs, o2, l2, dos)
+        torch.cuda.synchronize()
+        hq = slice(kv0 * G, (kv0 + n) * G)
+        for bi in range(cfg.batch):
+            nb = prob.seq_packed_len(bi)
+            assert torch.equal(o2[bi, :nb], o[bi, :nb, hq]) and torch.equal(l2[bi, :, :nb], lse[bi, hq, :nb])
+            assert torch.equal(dq2[bi, :nb], dq[bi, :nb, hq])
+            assert torch.equal(dk2[bi, :nb], dk[bi, :nb, kv0:kv0 + n])
+            assert torch.equal(dv2[bi, :nb], dv[bi, :nb, kv0:kv0 + n])

@@ -161,3 +161,45 @@ def test_fullsize_varlen_sampled(cuda_ok):
         mq = metrics(t2np(dq[b, rows, h]), dq_r)
         assert mq["finite"] and mq["rel_l2"] <= GRAD_REL_L2, (b, mq)
         assert torch.all(o[b, n_b:] == SENT) and torch.all(lse[b, :, n_b:] == SENT) and torch.all(dq[b, n_b:] == SENT)
+
+
+@pytest.mark.gpu
+def test_long_sequence_32k_sampled(cuda_ok):
+    """L = 32,768 (P 4,096 + R 28,672, Ntot 65,536, 512 q-tiles -- far past the
+    paper's 8k cap, P:229): sampled rows of O / LSE / dQ and sampled keys'
+    dK / dV vs the oracle; exercises the long column lists of the dK/dV
+    kernel and the tile map at NT = 512."""
+    from workloads import AttnConfig
+    cfg = AttnConfig("l32k", 1, 4, 1, 128, 4096, 28672, 4, seed=13)
+    prob = bd.Problem.from_cfg(cfg)
+    q, k, v, do = attn_inputs(cfg, device="cuda")
+    o, lse = bd.attn_fwd(prob, q, k, v)
+    dq, dk, dv = bd.attn_bwd(prob, q, k, v, o, lse, do)
+    torch.cuda.synchronize()
+    one = OProblem(1, cfg.prompt_len, cfg.response_len, cfg.block_size, 1, 1, cfg.head_dim, cfg.repeat_prompt)
+    L, N = cfg.L, cfg.ntot
+    rows = np.unique(np.concatenate([[0, L - 1, L, N - 1], np.random.default_rng(3).integers(0, N, 48)]))
+    for h in (0, 3):
+        qs, ks, vs, dos = (x[0:1, :, hh:hh + 1].float().cpu() for x, hh in ((q, h), (k, 0), (v, 0), (do, h)))
+        o_r, l_r = attention.forward_rows(one, qs, ks, vs, 0, 0, rows)
+        dq_r, _, _ = attention.backward_rows(one, qs, ks, vs, dos, 0, 0, rows)
+        mo = metrics(t2np(o[0, rows, h]), o_r)
+        assert mo["finite"] and mo["max_abs"] <= FWD_MAX_ABS and mo["rel_l2"] <= FWD_REL_L2, (h, mo)
+        assert metrics(t2np(lse[0, h, rows]), l_r)["max_abs"] <= FWD_MAX_ABS
+        mq = metrics(t2np(dq[0, rows, h]), dq_r)
+        assert mq["finite"] and mq["rel_l2"] <= GRAD_REL_L2, (h, mq)
+    # keys near the end of x0 and in xt: only the rows that see a key contribute to its dK / dV
+    keys = np.array([L - 1, L - 3 * cfg.block_size, L + 17, N - 1])
+    vis = mask.mask_rows(one, np.arange(N))[:, keys]
+    ks, vs = k[0:1, :, 0:1].float().cpu(), v[0:1, :, 0:1].float().cpu()
+    ref_dk = np.zeros((len(keys), cfg.head_dim))
+    ref_dv = np.zeros((len(keys), cfg.head_dim))
+    for h in range(4):
+        qs, dos = q[0:1, :, h:h + 1].float().cpu(), do[0:1, :, h:h + 1].float().cpu()
+        for j in range(len(keys)):
+            rr = np.where(vis[:, j])[0]
+            _, dk_p, dv_p = attention.backward_rows(one, qs, ks, vs, dos, 0, 0, rr)
+            ref_dk[j] += dk_p[keys[j]]
+            ref_dv[j] += dv_p[keys[j]]
+    assert metrics(t2np(dk[0, keys, 0]), ref_dk)["rel_l2"] <= GRAD_REL_L2
+    assert metrics(t2np(dv[0, keys, 0]), ref_dv)["rel_l2"] <= GRAD_REL_L2
