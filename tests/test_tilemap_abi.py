@@ -166,3 +166,25 @@ def test_row_length_within_capacity_stride_random():
         NT, maxrow = img[4], img[7]
         cap = (len(img) - 16 - 2 * (NT + 1) - 2 * NT) // 2
         assert maxrow <= cap // NT, (P, R, B, rp, S, maxrow, cap // NT)
+
+
+@pytest.mark.parametrize("name", ["sdar_8b", "sweep_b4", "sweep_b8", "sweep_b16", "sweep_b32"])
+def test_tilemap_bj_configs_vs_oracle_dense(name):
+    """bd_tilemap_dump equals the classification read off the
+    oracle's dense mask at every BASELINE attention config (SDAR-8B: the full
+    18,432^2 mask; SDAR-1.7B above)."""
+    cfg = CONFIGS[name]
+    got = bd.tilemap_dump(bd.Problem.from_cfg(cfg))
+    ref = tilemap.classify(OProblem(1, cfg.prompt_len, cfg.response_len, cfg.block_size, 1, 1, cfg.head_dim))
+    assert got == ref
+
+
+def test_tilemap_varlen_sequences_vs_oracle_dense():
+    """sdar_8b_varlen: the per-sequence maps are those of each sequence's own
+    (P, R_i) -- shortest, median and longest rollout checked dense."""
+    cfg = CONFIGS["sdar_8b_varlen"]
+    lens = sorted(cfg.resp_lens)
+    for R in (lens[0], lens[len(lens) // 2], lens[-1]):
+        got = bd.tilemap_dump(bd.Problem(1, cfg.prompt_len, R, cfg.block_size, 1, 1, 128))
+        ref = tilemap.classify(OProblem(1, cfg.prompt_len, R, cfg.block_size, 1, 1, 128))
+        assert got == ref, R
