@@ -17,7 +17,7 @@ out = {
     "attn_bwd_dq_kernel": tot(lambda n: n.startswith("attn_bwd_dq")),
     "logprob_ratio": tot(lambda n: n == "logprob_kernel") / (2048 * 151936 * 2),
     "logprob_bwd_ratio": tot(lambda n: n == "logprob_bwd_kernel") / (2 * 2048 * 151936 * 2),
-    "logprob_fused_ratio": tot(lambda n: n == "logprob_fused_kernel") / (2 * 2048 * 151936 * 2),
+    "logprob_fused_ratio": tot(lambda n: n.startswith("logprob_fused")) / (2 * 2048 * 151936 * 2),
 }
 json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)
 print(out)

@@ -155,3 +155,36 @@ def test_fused_logprob_masked_vocab(cuda_ok):
     assert np.isfinite(d).all()
     assert (d[~np.isfinite(t2np(z))] == 0).all()
     assert metrics(d, ref_dz)["rel_l2"] <= DZ_REL_L2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("low", [-60.0, -200.0])
+def test_fused_logprob_wide_spread(cuda_ok, low):
+    """The fused kernel takes each thread's FIRST vector's max as its exponent
+    reference and redoes the thread from global memory against its exact max
+    when a later element lies so far above it that the thread's sum leaves
+    [0, 2^64).  Rows whose every slice starts with 8 KB of very low logits
+    (every thread's first vector) followed by N(0, 3^2) logits and a +40 spike
+    take that path for every thread; a -inf-led row and a row with the spike
+    in the first vectors take the common path.  Element-wise vs the oracle."""
+    n, V = 6, VOCAB_QWEN3
+    z, t = logits_inputs(n, V, seed=31)
+    q = V // 4
+    for r in range(4):
+        for c in range(4):
+            z[r, c * q:c * q + 2048] = low  # bf16-exact for both values
+        z[r, (r * 7919 + 5000) % V] = 40.0
+    z[4, :2048] = float("-inf")
+    z[5, 100] = 40.0
+    w = torch.randn(n, generator=torch.Generator().manual_seed(8), dtype=torch.float32)
+    zc = z.cuda()
+    logp, lse, dz = ops.logprob(zc, t.cuda(), dlogp=w.cuda())
+    torch.cuda.synchronize()
+    ref_lp, ref_lse = olp.logprob(z, t.long())
+    ref_dz = olp.logprob_grad(z, t.long(), w.double().numpy())
+    assert metrics(t2np(logp), ref_lp)["max_abs"] <= LOGP_MAX_ABS
+    assert metrics(t2np(lse), ref_lse)["max_abs"] <= LOGP_MAX_ABS
+    d = t2np(dz)
+    assert np.isfinite(d).all()
+    for i in range(n):
+        assert metrics(d[i:i + 1], ref_dz[i:i + 1])["rel_l2"] <= DZ_REL_L2, i
