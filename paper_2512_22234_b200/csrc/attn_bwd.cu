@@ -798,6 +798,12 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
           for (int kv = 0; kv < 2; ++kv) {
             const int stage = dq_ring_slot<C>(2 * jg + kv);
             mbar_wait(&kv_empty[stage], dq_ring_phase<C>(2 * jg + kv) ^ 1);
+#ifdef BD_DQ_T_NOKV  // timing-only build: K / V loaded once per ring slot, never again (wrong results)
+            if (jg >= C::kStages) {
+              mbar_arrive(&kv_full[stage]);
+              continue;
+            }
+#endif
             mbar_expect_tx(&kv_full[stage], C::kTileBytes);
             uint8_t* dst = sRing + stage * C::kTileBytes;
             for (int kb = 0; kb < D / 64; ++kb)
@@ -932,6 +938,17 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
         const uint32_t sbase = tbase + lane_off + ((jg & 1) ? C::kColS1 : C::kColS0);
         mbar_wait(&s_full[jg & 1], (uint32_t)((jg >> 1) & 1));
         tc_fence_after();
+#ifdef BD_DQ_T_NOCOMP  // timing-only build: no TMEM traffic or math in the compute warps (wrong results)
+        (void)need_mask; (void)lo; (void)hi; (void)sbase;
+        mbar_wait(dp_full, (uint32_t)(jg & 1));
+        tc_fence_after();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dp_free);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&compute_done[jg & 1]);
+        continue;
+#endif
         float pv[32];
         {
           uint32_t sr[32];
