@@ -241,6 +241,10 @@ constexpr int kCl = 4;
 #define BD_LP_THREADS 256
 #endif
 constexpr int kFusedThreads = BD_LP_THREADS;
+#ifndef BD_LP_REGV
+#define BD_LP_REGV 5
+#endif
+constexpr int kLpRegV = BD_LP_REGV;  // register-held vectors per thread (see logprob_fused1p_kernel)
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -294,6 +298,12 @@ __device__ __forceinline__ uint4 exp_vec(const uint4& u, float2 nm2, float2& acc
   return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
+// REGV vectors per thread of the slice's tail are held in registers (plain
+// 16-byte streaming loads issued at entry) instead of shared memory: at the
+// Qwen3 vocabulary the slice's shared-memory part drops from 74 to 54 KB, so
+// four CTAs (instead of three) fit an SM and a third more of each SM's bytes
+// are in flight while the others compute (REGV = 0: the whole slice in smem).
+template <int REGV>
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
     logprob_fused1p_kernel(int V, const __nv_bfloat16* z, int64_t stride, const int32_t* __restrict__ targets,
                            float* __restrict__ logp, float* __restrict__ lse_out, const float* __restrict__ dlogp,
@@ -307,49 +317,79 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
   const uint32_t crank = cluster_rank();
   const int tid = threadIdx.x;
   const int Vc = V / kCl;
-  const int nv = Vc / 8;  // uint4 vectors in this slice
+  const int nv = Vc / 8;                        // uint4 vectors in this slice
+  const int nvs = nv - REGV * kFusedThreads;    // ... of which in shared memory: [0, nvs)
   const __nv_bfloat16* src = z + row * stride + (int64_t)crank * Vc;
+  const uint4* g4 = reinterpret_cast<const uint4*>(src);
   uint4* buf4 = reinterpret_cast<uint4*>(smem);
   if (tid == 0) {
     mbar_init(&bar, 1);
     mbar_init(&pbar, 1);
     fence_barrier_init();
   }
+  // the row's scalars and the register part of the slice go out first: their
+  // latency overlaps the bulk copy
+  const int t = targets[row];
+  const float wgt = dlogp ? dlogp[row] : 0.f;
+  uint4 rv[REGV > 0 ? REGV : 1];
+#pragma unroll
+  for (int k = 0; k < REGV; ++k) {
+    const ulonglong2 u = ld_stream(g4 + nvs + k * kFusedThreads + tid);
+    rv[k] = make_uint4((uint32_t)u.x, (uint32_t)(u.x >> 32), (uint32_t)u.y, (uint32_t)(u.y >> 32));
+  }
   __syncthreads();
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   if (tid == 0) {
-    const uint32_t bytes = (uint32_t)Vc * 2;
+    const uint32_t bytes = (uint32_t)nvs * 16;
     mbar_expect_tx(&bar, bytes);
     for (uint32_t off = 0; off < bytes; off += 32768) {
       const uint32_t n = bytes - off < 32768 ? bytes - off : 32768;
       bulk_load(smem + off, reinterpret_cast<const uint8_t*>(src) + off, n, &bar);
     }
   }
-  const int t = targets[row];
   const int tl = t - (int)crank * Vc;  // target within this slice (may fall outside)
   const int tv = (tl >= 0 && tl < Vc) ? tl >> 3 : -1;
+  // the target vector's owner: smem vector tv (thread tv % 256) or register
+  // vector k of thread (tv - nvs) % 256
+  const bool t_in_regs = tv >= nvs;
+  const int t_owner = tv < 0 ? -1 : (t_in_regs ? (tv - nvs) & (kFusedThreads - 1) : tv & (kFusedThreads - 1));
+  const int t_k = t_in_regs ? (tv - nvs) / kFusedThreads : -1;
+  if (REGV > 0 && t_in_regs && tid == t_owner) {
+    const int kk = tl & 7;
+#pragma unroll
+    for (int k = 0; k < REGV; ++k)
+      if (k == t_k) {
+        const uint32_t wd = (kk >> 1) == 0 ? rv[k].x : (kk >> 1) == 1 ? rv[k].y : (kk >> 1) == 2 ? rv[k].z : rv[k].w;
+        zt = __uint_as_float((kk & 1) ? (wd & 0xFFFF0000u) : (wd << 16));
+      }
+  }
   mbar_wait(&bar, 0);
-  if (tv >= 0 && tid == (tv & (kFusedThreads - 1)))
+  if (!t_in_regs && tv >= 0 && tid == t_owner)
     zt = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(smem)[tl]);  // read before the pass overwrites it
   // one pass: e against the thread's reference m_t (max of its first vector)
-  float mref = tid < nv ? vec_max(buf4[tid]) : -INFINITY;
+  float mref = tid < nvs ? vec_max(buf4[tid]) : -INFINITY;
   float m_t = mref == -INFINITY ? 0.f : mref;
   float2 acc = make_float2(0.f, 0.f);
   {
     const float2 nm2 = make_float2(-m_t * kLog2e, -m_t * kLog2e);
-    for (int i = tid; i < nv; i += kFusedThreads) buf4[i] = exp_vec(buf4[i], nm2, acc);
+    for (int i = tid; i < nvs; i += kFusedThreads) buf4[i] = exp_vec(buf4[i], nm2, acc);
+#pragma unroll
+    for (int k = 0; k < REGV; ++k) rv[k] = exp_vec(rv[k], nm2, acc);
   }
   float s_t = acc.x + acc.y;
   if (!(s_t < 18446744073709551616.f)) {
     // rare: an element far above the reference -- redo against the exact max
     // from the logits in global memory (this thread's vectors only)
-    const uint4* g4 = reinterpret_cast<const uint4*>(src);
     float mx = -INFINITY;
-    for (int i = tid; i < nv; i += kFusedThreads) mx = fmaxf(mx, vec_max(g4[i]));
+    for (int i = tid; i < nvs; i += kFusedThreads) mx = fmaxf(mx, vec_max(g4[i]));
+#pragma unroll
+    for (int k = 0; k < REGV; ++k) mx = fmaxf(mx, vec_max(g4[nvs + k * kFusedThreads + tid]));
     m_t = mx == -INFINITY ? 0.f : mx;
     const float2 nm2 = make_float2(-m_t * kLog2e, -m_t * kLog2e);
     acc = make_float2(0.f, 0.f);
-    for (int i = tid; i < nv; i += kFusedThreads) buf4[i] = exp_vec(g4[i], nm2, acc);
+    for (int i = tid; i < nvs; i += kFusedThreads) buf4[i] = exp_vec(g4[i], nm2, acc);
+#pragma unroll
+    for (int k = 0; k < REGV; ++k) rv[k] = exp_vec(g4[nvs + k * kFusedThreads + tid], nm2, acc);
     s_t = acc.x + acc.y;
   }
   // (reference, sum) pairs: warp shuffles, the CTA's warps, then the cluster
@@ -392,15 +432,13 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
   }
   if (!dlogp) return;
   // pass 2: dz = w (1[v = t] - e 2^(m_t - M) / sum)
-  const float wgt = dlogp[row];
   const float scl = wgt * ex2_approx((m_t - mg) * kLog2e) / tot;
   uint4* out = reinterpret_cast<uint4*>(dz + row * dz_stride + (int64_t)crank * Vc);
   const float nscl = -scl;
   const __nv_bfloat16 hi = __float2bfloat16_rn(nscl);
   const __nv_bfloat16 lo = __float2bfloat16_rn(nscl - __bfloat162float(hi));
   const __nv_bfloat162 hi2 = __halves2bfloat162(hi, hi), lo2 = __halves2bfloat162(lo, lo);
-  for (int i = tid; i < nv; i += kFusedThreads) {
-    const uint4 u = buf4[i];
+  auto grad_vec = [&](const uint4& u, int i) {
     uint32_t w[4] = {u.x, u.y, u.z, u.w};
     if (i != tv) {
 #pragma unroll
@@ -419,7 +457,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kFusedThreads)
       }
     }
     out[i] = make_uint4(w[0], w[1], w[2], w[3]);
-  }
+  };
+  for (int i = tid; i < nvs; i += kFusedThreads) grad_vec(buf4[i], i);
+#pragma unroll
+  for (int k = 0; k < REGV; ++k) grad_vec(rv[k], nvs + k * kFusedThreads + tid);
 }
 
 }  // namespace
@@ -459,13 +500,17 @@ extern "C" int bd_logprob(int64_t n_rows, int32_t vocab, const void* logits, int
   const bool fusable = dlogp && vocab % (8 * kCl) == 0 && row_stride % 8 == 0 && dlogits_stride % 8 == 0 &&
                        aligned16(logits) && aligned16(dlogits) && (int64_t)n_rows * kCl <= 0x7FFFFFFF;
   if (fusable) {
-    // one HBM read + one HBM write: the row stays in the cluster's shared memory
-    const int smem = vocab / kCl * 2;
-    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(logprob_fused1p_kernel), 200 * 1024,
+    // one HBM read + one HBM write: the row stays in the cluster's shared
+    // memory (the tail of each slice in registers when the slice is large)
+    const int nv = vocab / kCl / 8;
+    const bool regs = nv >= (kLpRegV + 1) * kFusedThreads;
+    const int smem = (nv - (regs ? kLpRegV * kFusedThreads : 0)) * 16;
+    if (smem > 200 * 1024) return set_error(BD_ERR_UNSUPPORTED, "vocab too large for the fused path");
+    auto kern = regs ? logprob_fused1p_kernel<kLpRegV> : logprob_fused1p_kernel<0>;
+    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), 200 * 1024,
                                   "cudaFuncSetAttribute(logprob_fused1p)"))
       return rc;
-    if (smem > 200 * 1024) return set_error(BD_ERR_UNSUPPORTED, "vocab too large for the fused path");
-    logprob_fused1p_kernel<<<(unsigned)(n_rows * kCl), kFusedThreads, smem, stream>>>(
+    kern<<<(unsigned)(n_rows * kCl), kFusedThreads, smem, stream>>>(
         vocab, reinterpret_cast<const __nv_bfloat16*>(logits), row_stride, targets, logp, lse, dlogp,
         reinterpret_cast<__nv_bfloat16*>(dlogits), dlogits_stride);
     note_launches(1);

@@ -188,3 +188,30 @@ def test_fused_logprob_wide_spread(cuda_ok, low):
     assert np.isfinite(d).all()
     for i in range(n):
         assert metrics(d[i:i + 1], ref_dz[i:i + 1])["rel_l2"] <= DZ_REL_L2, i
+
+
+@pytest.mark.gpu
+def test_fused_logprob_target_positions(cuda_ok):
+    """Targets at slice edges and inside the register-held tail of the fused
+    kernel's slices (at Qwen3 V the last 1,280 vectors of every 37,984-element
+    slice live in registers, the rest in shared memory): logp, LSE and dz
+    element-wise vs the oracle, the target entry included."""
+    V = VOCAB_QWEN3
+    q = V // 4
+    tail0 = q - 1280 * 8  # first register-held element of a slice
+    pos = [0, 7, 8, tail0 - 1, tail0, tail0 + 9, q - 1, q, 2 * q + tail0 + 3, 3 * q - 1, V - 8, V - 1]
+    n = len(pos)
+    z, _ = logits_inputs(n, V, seed=41)
+    t = torch.tensor(pos, dtype=torch.int32)
+    w = torch.randn(n, generator=torch.Generator().manual_seed(9), dtype=torch.float32)
+    logp, lse, dz = ops.logprob(z.cuda(), t.cuda(), dlogp=w.cuda())
+    torch.cuda.synchronize()
+    ref_lp, ref_lse = olp.logprob(z, t.long())
+    ref_dz = olp.logprob_grad(z, t.long(), w.double().numpy())
+    assert metrics(t2np(logp), ref_lp)["max_abs"] <= LOGP_MAX_ABS
+    assert metrics(t2np(lse), ref_lse)["max_abs"] <= LOGP_MAX_ABS
+    d = t2np(dz)
+    for i in range(n):
+        assert metrics(d[i:i + 1], ref_dz[i:i + 1])["rel_l2"] <= DZ_REL_L2, i
+        # the target entry itself: w (1 - p_t) within bf16 rounding
+        assert abs(d[i, pos[i]] - ref_dz[i, pos[i]]) <= 1e-2 * abs(w[i].item()) + 1e-3, (i, d[i, pos[i]], ref_dz[i, pos[i]])
