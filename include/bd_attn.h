@@ -110,7 +110,15 @@ int64_t bd_packed_len(const bd_problem* prob);
 /* Workspace bytes needed by bd_attn_fwd (backward = 0) or bd_attn_bwd
  * (backward = 1).  The forward workspace holds the tile map; the backward
  * one additionally holds D = rowsum(dO * O) and the log2-scaled LSE, fp32,
- * tile-major [b, Hq, n_tiles, 128].  Returns 0 for an invalid problem. */
+ * tile-major [b, Hq, n_tiles, 128], and -- for uniform (non-varlen) batches
+ * -- when BD_BWD_DS=1 (env; off by default) the stored-dS buffer: bf16 dS^T
+ * of every visible 128x128 tile of one chunk of sequences, Hq *
+ * bd_tilemap_entries_bound(prob) * 32 KB per sequence, as many sequences
+ * per chunk as fit BD_BWD_DS_BUDGET_MB (env, default 24,576 MiB; SDAR-8B:
+ * 4 sequences, 22.3 GB).  Off, or one sequence over the budget: no buffer,
+ * dQ recomputes S and dP.
+ * The environment is read per call: keep it fixed between the workspace
+ * query and the call.  Returns 0 for an invalid problem. */
 size_t bd_attn_workspace_bytes(const bd_problem* prob, int backward);
 
 /* Forward.
@@ -129,9 +137,12 @@ int bd_attn_fwd(const bd_problem* prob, const void* q, const void* k, const void
 /* Backward of bd_attn_fwd for upstream gradient dout (bf16, like q), given the
  * forward's o and lse.  Writes dq (bf16 like q) and dk, dv (bf16 like k); dk
  * and dv sum over the Hq/Hkv query heads of each kv head.  ws must be
- * >= bd_attn_workspace_bytes(prob, 1) bytes.  Three kernels (preprocess,
- * dK/dV over the column tile map, dQ over the row tile map); no atomics, so
- * the result is deterministic. */
+ * >= bd_attn_workspace_bytes(prob, 1) bytes.  Kernels: preprocess, dK/dV
+ * over the column tile map, dQ over the row tile map (recomputing S and dP).
+ * With the stored-dS buffer (BD_BWD_DS=1, see bd_attn_workspace_bytes), per
+ * chunk of sequences the dK/dV kernel also stores each tile's dS^T = P (dP -
+ * D), bf16 (the value its dK MMA consumes), and dQ = scale dS K reads it back
+ * instead of recomputing.  No atomics: the result is deterministic. */
 int bd_attn_bwd(const bd_problem* prob, const void* q, const void* k, const void* v, const void* o,
                 const float* lse, const void* dout, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
                 void* stream);
@@ -271,6 +282,12 @@ int bd_tilemap_dump(const bd_problem* prob, int32_t* host_out, size_t cap, int64
 /* Tile-map statistics (host): counts of q-tiles, non-empty, FULL and PARTIAL
  * tiles per (sequence, head); out = int64[4]. */
 int bd_tilemap_stats(const bd_problem* prob, int64_t* out);
+
+/* Number of non-empty tiles per (sequence, head) computed from the candidate
+ * ranges alone (O(NT); tilemap.cuh map_entries_bound): the per-(sequence,
+ * q-head) stride of the stored dS^T tiles in the backward workspace.  Equals
+ * bd_tilemap_stats' out[1] (tests check it); -1 on an invalid problem. */
+int64_t bd_tilemap_entries_bound(const bd_problem* prob);
 
 /* Diagnostic (host): checks that the per-row visible-key intervals used by the
  * forward/dQ kernels and the per-key visible-row intervals used by the dK/dV

@@ -52,6 +52,7 @@ SIGNATURES = {
     "bd_dipo_token_loss": (ctypes.c_int, [_I64, _P, _P, _P, _I32, _P, _P, _P, _I32, _I32, _F, _P, _P, _P]),
     "bd_tilemap_dump": (ctypes.c_int, [_PROB, ctypes.POINTER(_I32), _SZ, ctypes.POINTER(_I64)]),
     "bd_tilemap_stats": (ctypes.c_int, [_PROB, ctypes.POINTER(_I64)]),
+    "bd_tilemap_entries_bound": (_I64, [_PROB]),
     "bd_tilemap_selfcheck": (ctypes.c_int, [_PROB, ctypes.POINTER(_I64)]),
     "bd_mask_dump": (ctypes.c_int, [_PROB, _I32, _I64, _I64, _P, _SZ, ctypes.POINTER(_I64)]),
     "bd_error_string": (ctypes.c_char_p, [ctypes.c_int]),

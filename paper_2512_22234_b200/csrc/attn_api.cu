@@ -9,8 +9,10 @@ namespace {
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
-  size_t map_off, dsum_off, total;
+  size_t map_off, dsum_off, ds_off, ds_bytes, total;
   int map_stride;  // words between per-sequence maps (varlen), 0 = one map
+  long long ds_stride;
+  int ds_chunk;
 };
 
 WsLayout ws_layout(const bd_problem& p, int backward) {
@@ -23,6 +25,9 @@ WsLayout ws_layout(const bd_problem& p, int backward) {
   if (backward) {
     w.dsum_off = off;  // tile-major log2-LSE and D vectors (dQ accumulates in TMEM)
     off = align256(off + bwd_vec_floats(p, g) * sizeof(float));
+    w.ds_bytes = ds_plan_bytes(p, g, &w.ds_stride, &w.ds_chunk);  // stored dS^T tiles (one chunk)
+    w.ds_off = off;
+    off = align256(off + w.ds_bytes);
   }
   w.total = off;
   return w;
@@ -92,6 +97,12 @@ extern "C" int bd_attn_bwd(const bd_problem* prob, const void* q, const void* k,
   char* w = static_cast<char*>(ws);
   int* map = reinterpret_cast<int*>(w + wl.map_off);
   if ((rc = build_maps(*prob, g, wl, map, stream))) return rc;
+  DsPlan ds;
+  if (wl.ds_bytes) {
+    ds.buf = w + wl.ds_off;
+    ds.stride = wl.ds_stride;
+    ds.chunk = wl.ds_chunk;
+  }
   return run_attn_bwd(*prob, g, q, k, v, o, lse, dout, dq, dk, dv, map, wl.map_stride,
-                      reinterpret_cast<float*>(w + wl.dsum_off), stream);
+                      reinterpret_cast<float*>(w + wl.dsum_off), ds, stream);
 }

@@ -130,6 +130,11 @@ struct BwdArgs {
   Geom g;
   float scale, scale_log2;
   int trace;  // 1 = record the trace for blockIdx.x == 0
+  // stored-dS path: the dK/dV kernel writes every tile's dS^T (bf16,
+  // [128 keys][128 q]) at tile slot (b Hq + h) ds_stride + (its row-CSR entry
+  // index), the dQ kernel reads each q-tile's row of tiles contiguously
+  __nv_bfloat16* ds;  // null: dQ recomputes S and dP (attn_bwd_dqp_kernel)
+  long long ds_stride;
 };
 
 __device__ __forceinline__ void store_row_bf16(__nv_bfloat16* dst, const uint32_t* v, float mul, bool ok) {
@@ -491,11 +496,17 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
     // whole q-tile ahead (its global-load latency stays off the compute path)
     int hs = 0, eidx = n_qt - 1;
     int ent_next = n_it > 0 ? ents[eidx] : 0;
+    const int* rposv = mv.col_rpos() + e0;  // row-CSR index of each column entry (stored-dS slots)
+    int rpos_next = (a.ds && n_it > 0) ? rposv[eidx] : 0;
     for (int i = 0; i < n_it; ++i) {
       const int ent = ent_next;
+      const int rpos = rpos_next, hcur = hs;
       if (++hs == a.group) {
         hs = 0;
-        if (--eidx >= 0) ent_next = ents[eidx];
+        if (--eidx >= 0) {
+          ent_next = ents[eidx];
+          if (a.ds) rpos_next = rposv[eidx];
+        }
       }
       const int qt = entry_tile(ent);
       int q0, q1, qseg;
@@ -560,13 +571,28 @@ __global__ void __launch_bounds__(DkdvCfg<D>::kThreads, 1)
             if (lane == 0) mbar_arrive(&pt_half[wg]);
           }
         }
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&pt_done[wg]);  // this warpgroup's P^T(i), dS^T(i) written: its dV(i), dK(i) k-steps may issue
-        mbar_arrive(&vec_empty[i & 1]);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&pt_done[wg]);  // this warpgroup's P^T(i), dS^T(i) written: its dV(i), dK(i) k-steps may issue
+          mbar_arrive(&vec_empty[i & 1]);
+        }
+        if (a.ds) {
+          // this key row's 32 q columns of dS^T(i) -> its tile slot (64 B),
+          // after the arrive (off the MMA chain), streaming (evict-first) so
+          // the Q / dO tiles the group's CTAs share stay in L2
+          // tile layout: 16 chunks of 8 q columns, each [128 keys][8 q] (16 B
+          // per key) -- the no-swizzle MN-major UMMA layout of the dQ
+          // kernel's A operand, and each warp's store u is 512 contiguous bytes
+          const long long slot = ((long long)b * a.n_q_heads + kvh * a.group + hcur) * a.ds_stride + rpos;
+          __nv_bfloat16* dst = a.ds + slot * (kTileRows * kTileRows) + ((4 * wg) * kTileRows + r) * 8;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(dst + u * kTileRows * 8),
+                         "r"(dsk[4 * u]), "r"(dsk[4 * u + 1]), "r"(dsk[4 * u + 2]), "r"(dsk[4 * u + 3])
+                         : "memory");
+        }
       }
       TRACE(8 * (i & 127) + 4, blockIdx.x == 0 && threadIdx.x == 0);
     }
@@ -1018,10 +1044,156 @@ int set_smem(K kernel, int bytes) {
   return ensure_smem_attr(reinterpret_cast<const void*>(kernel), bytes, "cudaFuncSetAttribute(bwd)");
 }
 
+// ========================================================= dQ from stored dS
+// dQ = scale dS K over a q-tile's row of tiles, dS^T read from the workspace
+// where the dK/dV kernel stored it (BwdArgs::ds): no S / dP recompute, no
+// exps -- 2 d FLOP per visible pair instead of 6 d, and the kernel streams
+// each tile's 32 KB of dS^T once from HBM (the K tiles, shared by the
+// group's heads and the sequence's q-tiles, come from L2).  Persistent: one
+// CTA per SM walks the dQ units in the same order as attn_bwd_dqp_kernel.
+// Warps 0-3: epilogue (TMEM lane quarters); warp 4: TMA; warp 5: MMA.
+// TMEM: two D-column dQ accumulators (unit u in buffer u & 1), so a unit's
+// drain overlaps the next unit's MMAs.
+template <int D>
+struct DqDsCfg {
+  // dS^T tile, bf16: 16 chunks of 8 q columns, each [128 keys][8 q] (the
+  // no-swizzle MN-major A layout; one 32 KB bulk copy per tile)
+  static constexpr int kDsBytes = kTileRows * kTileRows * 2;
+  static constexpr int kKBytes = kTileRows * D * 2;
+  static constexpr int kStageBytes = kDsBytes + kKBytes;
+  static constexpr int kStages = D == 128 ? 3 : 4;
+  static constexpr int kTmaWarp = 4, kMmaWarp = 5;
+  static constexpr int kThreads = 6 * 32;
+  static constexpr uint32_t kTmemCols = 2 * D;
+  static constexpr int kOffBar = kStages * kStageBytes;
+  // full[S], empty[S], acc_full[2], acc_empty[2]
+  static constexpr int kNumBars = 2 * kStages + 4;
+  static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16;
+  static_assert(kSmemBytes <= 232448, "dq-ds smem budget");
+};
+
+template <int D>
+__global__ void __launch_bounds__(DqDsCfg<D>::kThreads, 1)
+    attn_bwd_dq_ds_kernel(const __grid_constant__ CUtensorMap tmK, const BwdArgs a, int n_units) {
+  using C = DqDsCfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* full = bars;
+  uint64_t* empty = full + C::kStages;
+  uint64_t* acc_full = empty + C::kStages;  // [2]
+  uint64_t* acc_empty = acc_full + 2;       // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
+  const int warp = (int)warp_id(), lane = (int)lane_id();
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
+  if (warp == 0) tmem_alloc<C::kTmemCols>(tslot);
+  if (warp == C::kTmaWarp && lane == 0) {
+    for (int i = 0; i < C::kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 4);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmK);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const MapView mv{const_cast<int*>(a.map), a.g.NT, map_capacity(a.g)};
+
+  if (warp == C::kTmaWarp) {
+    // ================================================================ TMA
+    if (elect_one()) {
+      int it = 0;  // tiles issued by this CTA
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const DqUnit w = dq_unit<false>(a, u);
+        const int kvh = w.h / a.group;
+        const long long slot0 = ((long long)w.b * a.n_q_heads + w.h) * a.ds_stride + mv.row_ptr()[w.qt];
+        for (int j = 0; j < w.n_kt; ++j, ++it) {
+          const int st = it % C::kStages;
+          mbar_wait(&empty[st], (uint32_t)(((it / C::kStages) & 1) ^ 1));
+          mbar_expect_tx(&full[st], C::kStageBytes);
+          uint8_t* dst = smem + st * C::kStageBytes;
+          bulk_load(dst, a.ds + (slot0 + j) * (kTileRows * kTileRows), C::kDsBytes, &full[st]);
+          const int k0 = tile_start(w.g, entry_tile(w.ents[j]));
+          for (int kb = 0; kb < D / 64; ++kb)
+            tma_load_4d(dst + C::kDsBytes + kb * 16384, &tmK, &full[st], kb * 64, kvh, k0, w.b);
+        }
+      }
+    }
+  } else if (warp == C::kMmaWarp) {
+    // ================================================================ MMA
+    if (elect_one()) {
+      // A = dS (M = q rows, K = keys): the stored dS^T tile is MN-major A;
+      // B = K (K = keys, N = d): MN-major B
+      constexpr uint32_t idesc = umma_idesc_bf16(128, D, true, true);
+      int it = 0, uu = 0;  // tiles consumed, units with tiles
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const DqUnit w = dq_unit<false>(a, u);
+        if (w.n_kt == 0) continue;
+        const int ab = uu & 1;
+        mbar_wait(&acc_empty[ab], (uint32_t)(((uu >> 1) & 1) ^ 1));
+        tc_fence_after();
+        const uint32_t acc = tbase + ab * D;
+        for (int j = 0; j < w.n_kt; ++j, ++it) {
+          const int st = it % C::kStages;
+          mbar_wait(&full[st], (uint32_t)((it / C::kStages) & 1));
+          tc_fence_after();
+          const uint32_t sds = smem_u32(smem + st * C::kStageBytes), sk = sds + C::kDsBytes;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            umma_ss(acc, umma_desc_noswz(sds + k * 256, 128, 2048), umma_desc_sw128(sk + k * 2048, 16384, 1024),
+                    idesc, (j > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&empty[st]);
+        }
+        umma_commit(&acc_full[ab]);
+        ++uu;
+      }
+    }
+  } else if (warp < 4) {
+    // =========================================================== epilogue
+    const int r = warp * 32 + lane;  // query row within the tile == TMEM lane
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    int uu = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const DqUnit w = dq_unit<false>(a, u);
+      const int row = w.q0 + r;
+      const bool ok = row < w.q1;
+      __nv_bfloat16* out = a.dq + (((size_t)w.b * a.N + row) * a.q_row_heads + w.h) * D;
+      if (w.n_kt == 0) {
+        uint32_t z[32] = {};
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) store_row_bf16(out + 32 * c, z, 0.f, ok);
+        continue;
+      }
+      const int ab = uu & 1;
+      mbar_wait(&acc_full[ab], (uint32_t)((uu >> 1) & 1));
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tbase + lane_off + ab * D + 32 * c, v);
+        tmem_ld_wait();
+        store_row_bf16(out + 32 * c, v, a.scale, ok);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[ab]);
+      ++uu;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<C::kTmemCols>(tbase);
+}
+
 template <int D, bool VARLEN>
 int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, const void* o,
                const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, int map_stride,
-               float* vec_ws, cudaStream_t stream) {
+               float* vec_ws, const DsPlan& ds, cudaStream_t stream) {
   const int Hq = p.n_q_heads;
   const size_t nvec = (size_t)p.batch * Hq * g.NT * kTileRows;
   float* lse2_t = vec_ws;
@@ -1045,6 +1217,7 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   int rc = set_smem(attn_bwd_dkdv_kernel<D, VARLEN>, DkdvCfg<D>::kSmemBytes);
   if (rc) return rc;
   if ((rc = set_smem(attn_bwd_dqp_kernel<D, VARLEN>, DqCfg<D>::kSmemBytes))) return rc;
+  if (!VARLEN && (rc = set_smem(attn_bwd_dq_ds_kernel<D>, DqDsCfg<D>::kSmemBytes))) return rc;
   BwdArgs a;
   a.map = map;
   a.map_stride = map_stride;
@@ -1065,6 +1238,51 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   a.scale_log2 = a.scale * kLog2e;
   static const int trace_on = getenv("BD_TRACE") ? atoi(getenv("BD_TRACE")) : 0;
   a.trace = trace_on;
+  a.ds = nullptr;
+  a.ds_stride = 0;
+  int n_sm = 0;
+  if ((rc = current_sm_count(&n_sm))) return rc;
+  if (!VARLEN && ds.buf) {
+    // stored-dS path, in chunks of ds.chunk sequences (the dS^T buffer holds
+    // one chunk): dK/dV(chunk) writes every tile's dS^T, dQ(chunk) reads it
+    const int Hkv = p.n_kv_heads;
+    int launches = 2;  // zero, pre
+    for (int s0 = 0; s0 < p.batch; s0 += ds.chunk) {
+      const int nb = p.batch - s0 < ds.chunk ? p.batch - s0 : ds.chunk;
+      const size_t qoff = (size_t)s0 * g.N * qrh * D, kvoff = (size_t)s0 * g.N * kvrh * D;
+      const auto* qb = reinterpret_cast<const __nv_bfloat16*>(q) + qoff;
+      const auto* kb = reinterpret_cast<const __nv_bfloat16*>(k) + kvoff;
+      const auto* vb = reinterpret_cast<const __nv_bfloat16*>(v) + kvoff;
+      const auto* dob = reinterpret_cast<const __nv_bfloat16*>(dout) + qoff;
+      CUtensorMap cQ, cK, cV, cDO;
+      if (!make_qkv_tmap(&cQ, qb, nb, g.N, Hq, D, 128, qrh) || !make_qkv_tmap(&cK, kb, nb, g.N, Hkv, D, 128, kvrh) ||
+          !make_qkv_tmap(&cV, vb, nb, g.N, Hkv, D, 128, kvrh) ||
+          !make_qkv_tmap(&cDO, dob, nb, g.N, Hq, D, 128, qrh))
+        return set_error(BD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+      BwdArgs c = a;
+      c.batch = nb;
+      c.lse2_t = lse2_t + (size_t)s0 * Hq * g.NT * kTileRows;
+      c.dsum_t = dsum_t + (size_t)s0 * Hq * g.NT * kTileRows;
+      c.dq = a.dq + qoff;
+      c.dk = a.dk + kvoff;
+      c.dv = a.dv + kvoff;
+      c.ds = reinterpret_cast<__nv_bfloat16*>(ds.buf);
+      c.ds_stride = ds.stride;
+      const long long grid_kv = (long long)g.NT * nb * Hkv;
+      attn_bwd_dkdv_kernel<D, VARLEN><<<(unsigned)grid_kv, DkdvCfg<D>::kThreads, DkdvCfg<D>::kSmemBytes, stream>>>(
+          cQ, cK, cV, cDO, c);
+      if ((rc = check_cuda(cudaGetLastError(), "attn_bwd_dkdv_kernel launch"))) return rc;
+      const long long units = (long long)g.NT * nb * Hq;
+      if (units > 0x7FFFFFFF) return set_error(BD_ERR_UNSUPPORTED, "grid too large");
+      const int grid_p = (int)(units < n_sm ? units : n_sm);
+      attn_bwd_dq_ds_kernel<D><<<(unsigned)grid_p, DqDsCfg<D>::kThreads, DqDsCfg<D>::kSmemBytes, stream>>>(
+          cK, c, (int)units);
+      if ((rc = check_cuda(cudaGetLastError(), "attn_bwd_dq_ds_kernel launch"))) return rc;
+      launches += 2;
+    }
+    note_launches(launches);
+    return BD_OK;
+  }
   // 2. dK, dV
   const long long grid_kv = (long long)g.NT * p.batch * p.n_kv_heads;
   attn_bwd_dkdv_kernel<D, VARLEN><<<(unsigned)grid_kv, DkdvCfg<D>::kThreads, DkdvCfg<D>::kSmemBytes, stream>>>(
@@ -1073,8 +1291,6 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
   // 3. dQ
   const long long grid_q = (long long)g.NT * p.batch * Hq;
   if (grid_q > 0x7FFFFFFF) return set_error(BD_ERR_UNSUPPORTED, "grid too large");
-  int n_sm = 0;
-  if ((rc = current_sm_count(&n_sm))) return rc;
   const int grid_p = (int)(grid_q < n_sm ? grid_q : n_sm);
   attn_bwd_dqp_kernel<D, VARLEN><<<(unsigned)grid_p, DqCfg<D>::kThreads, DqCfg<D>::kSmemBytes, stream>>>(
       tmQ, tmK, tmV, tmDO, a, (int)grid_q);
@@ -1084,17 +1300,34 @@ int launch_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k,
 
 }  // namespace
 
+size_t ds_plan_bytes(const bd_problem& p, const Geom& g, long long* stride, int* chunk) {
+  *stride = 0;
+  *chunk = 0;
+  // read per call (the workspace query and the launch of one call agree as
+  // long as the environment does not change in between)
+  const bool on = getenv("BD_BWD_DS") && atoi(getenv("BD_BWD_DS")) != 0;  // opt-in
+  const long long budget = (getenv("BD_BWD_DS_BUDGET_MB") ? atoll(getenv("BD_BWD_DS_BUDGET_MB")) : 24576LL) << 20;
+  if (!on || is_varlen(p) || p.batch <= 0) return 0;
+  const long long E = map_entries_bound(g);
+  const long long per_seq = (long long)p.n_q_heads * E * kTileRows * kTileRows * 2;
+  if (E <= 0 || per_seq > budget) return 0;
+  const long long c = budget / per_seq;
+  *chunk = (int)(c < p.batch ? c : p.batch);
+  *stride = E;
+  return (size_t)(*chunk) * (size_t)per_seq;
+}
+
 size_t bwd_vec_floats(const bd_problem& p, const Geom& g) {
   return 2 * (size_t)p.batch * p.n_q_heads * g.NT * kTileRows;
 }
 
 int run_attn_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, const void* o,
                  const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, int map_stride,
-                 float* vec_ws, cudaStream_t stream) {
+                 float* vec_ws, const DsPlan& ds, cudaStream_t stream) {
   const bool vl = map_stride != 0;
-#define BD_BWD_CASE(D_)                                                                                  \
-  return vl ? launch_bwd<D_, true>(p, g, q, k, v, o, lse, dout, dq, dk, dv, map, map_stride, vec_ws, stream) \
-            : launch_bwd<D_, false>(p, g, q, k, v, o, lse, dout, dq, dk, dv, map, map_stride, vec_ws, stream)
+#define BD_BWD_CASE(D_)                                                                                      \
+  return vl ? launch_bwd<D_, true>(p, g, q, k, v, o, lse, dout, dq, dk, dv, map, map_stride, vec_ws, ds, stream) \
+            : launch_bwd<D_, false>(p, g, q, k, v, o, lse, dout, dq, dk, dv, map, map_stride, vec_ws, ds, stream)
   if (p.head_dim == 128) BD_BWD_CASE(128);
   if (p.head_dim == 64) BD_BWD_CASE(64);
 #undef BD_BWD_CASE

@@ -25,9 +25,25 @@ int build_map_device_varlen(const Geom& gmax, const SeqLens& lens, int* ws, long
 // map_stride: words between consecutive sequences' maps (0 = one shared map)
 int run_attn_fwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, void* o,
                  float* lse, const int* map, int map_stride, cudaStream_t stream);
+// Stored-dS backward (uniform batches): the dK/dV kernel writes every
+// visible tile's dS^T (bf16, 32 KB) into `buf`, `stride` tiles per (sequence,
+// q-head) (map_entries_bound), and the dQ kernel reads it back -- in chunks of
+// `chunk` sequences, `buf` holding one chunk.  buf == nullptr: the dQ kernel
+// recomputes S and dP (varlen batches, or when disabled / over budget).
+struct DsPlan {
+  void* buf = nullptr;
+  long long stride = 0;
+  int chunk = 0;
+};
+// The plan's sizes for a problem (host, deterministic): bytes of the dS^T
+// buffer (0 = path off).  BD_BWD_DS=1 enables the path; BD_BWD_DS_BUDGET_MB
+// (default 24,576) caps the buffer, which then holds floor(budget / per
+// sequence) sequences (off if one sequence exceeds it).  Opt-in: BD_BWD_DS=1
+// (measured no faster than the recompute path on B200).
+size_t ds_plan_bytes(const bd_problem& p, const Geom& g, long long* stride, int* chunk);
 int run_attn_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, const void* o,
                  const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, int map_stride,
-                 float* vec_ws, cudaStream_t stream);
+                 float* vec_ws, const DsPlan& ds, cudaStream_t stream);
 size_t bwd_vec_floats(const bd_problem& p, const Geom& g);
 
 }  // namespace bd

@@ -192,6 +192,20 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo
   return d;
 }
 
+// Shared-memory matrix descriptor, no swizzle ("interleave" canonical layout
+// of 8-row x 16-byte core matrices).  MN-major operand: core matrix = 8
+// consecutive K rows of 8 MN elements (128 B contiguous); lbo = byte stride
+// between consecutive 8-row K groups, sbo = between consecutive 8-element MN
+// chunks.
+__device__ __forceinline__ uint64_t umma_desc_noswz(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version (sm_100); layout type 0 = SWIZZLE_NONE
+  return d;
+}
+
 // Instruction descriptor, kind::f16 with bf16 inputs and fp32 accumulate.
 __host__ __device__ constexpr uint32_t umma_idesc_bf16(uint32_t M, uint32_t N, bool a_mn, bool b_mn) {
   return (1u << 4)                // D format: f32

@@ -204,6 +204,10 @@ __host__ __device__ inline int entry_kind(int e) { return (e >> 28) & 0xF; }
 //   col_ent[cap]   q-tile | kind << 28, q-tiles in increasing order
 //   fwd_order[NT]  q-tiles by decreasing row length (longest first, LPT)
 //   bwd_order[NT]  k-tiles by decreasing column length
+//   col_rpos[cap]  for column entry c (of q-tile t, k-tile kt): the index e of
+//                  kt in the ROW CSR (row_ent[e]) -- where the dK/dV kernel
+//                  stores that tile's dS^T so the dQ kernel reads its row's
+//                  tiles contiguously
 constexpr int kMapMagic = 0x42444D31;  // "BDM1"
 constexpr int kMapHeader = 16;  // [8] = S (noisy copies); [9] = sequence (varlen); [10..15] reserved
 
@@ -216,6 +220,7 @@ struct MapView {
   __host__ __device__ int* col_ent() const { return col_ptr() + NT + 1; }
   __host__ __device__ int* fwd_order() const { return col_ent() + cap; }
   __host__ __device__ int* bwd_order() const { return fwd_order() + NT; }
+  __host__ __device__ int* col_rpos() const { return bwd_order() + NT; }
 };
 
 // Upper bound on entries: a q-tile lists at most T0 x0 tiles and xt_max tiles
@@ -229,7 +234,27 @@ __host__ __device__ inline int map_capacity(const Geom& g) {
   return g.NT * (g.T0 + (xt_max < g.T1 ? xt_max : g.T1));
 }
 __host__ __device__ inline long long map_words(const Geom& g) {
-  return (long long)kMapHeader + 2LL * (g.NT + 1) + 2LL * map_capacity(g) + 2LL * g.NT;
+  return (long long)kMapHeader + 2LL * (g.NT + 1) + 3LL * map_capacity(g) + 2LL * g.NT;
+}
+
+// Number of listed (q-tile, k-tile) pairs, from the candidate ranges alone
+// (O(NT), host side): every candidate tile is non-empty -- a row's x0
+// interval starts at key 0 and the own-copy intervals of a tile's rows are
+// whole adjacent blocks, so the union over the tile's rows is one interval
+// per segment and each tile overlapping it holds a key some row sees -- so
+// this equals the builder's n_entries; it is used as an upper bound (the
+// per-(sequence, head) stride of the stored dS^T tiles) either way.
+__host__ __device__ inline long long map_entries_bound(const Geom& g) {
+  long long n = 0;
+  for (int t = 0; t < g.NT; ++t) {
+    const int qs = tile_seg(g, t);
+    for (int kk = 0; kk < (qs ? 2 : 1); ++kk) {
+      int a, b;
+      candidate_range(g, t, kk ? qs : 0, a, b);
+      n += b - a;
+    }
+  }
+  return n;
 }
 
 // Geometry of the sequence whose map starts at `base` (varlen batches keep

@@ -55,6 +55,7 @@ void build_map_host(const Geom& g, std::vector<int>& w) {
   for (int t = 0; t < g.NT; ++t)
     for (int e = mv.row_ptr()[t]; e < mv.row_ptr()[t + 1]; ++e) {
       const int kt = entry_tile(mv.row_ent()[e]);
+      mv.col_rpos()[mv.col_ptr()[kt] + fill[kt]] = e;
       mv.col_ent()[mv.col_ptr()[kt] + fill[kt]++] = entry_make(t, entry_kind(mv.row_ent()[e]));
     }
   std::vector<int> ord(g.NT);
@@ -251,6 +252,7 @@ __device__ void build_map_body(const Geom& g, int* __restrict__ ws, int seq, int
         for (int i = lane; i < n; i += 32) {
           const int ent = s_ent[t * stride + i];
           const int kt = entry_tile(ent);
+          mv.col_rpos()[s_cp[kt] + colfill[kt]] = mv.row_ptr()[t] + i;
           mv.col_ent()[s_cp[kt] + colfill[kt]++] = entry_make(t, entry_kind(ent));
         }
       } else {
@@ -258,6 +260,7 @@ __device__ void build_map_body(const Geom& g, int* __restrict__ ws, int seq, int
         for (int e = e0 + lane; e < e1; e += 32) {
           const int ent = mv.row_ent()[e];
           const int kt = entry_tile(ent);
+          mv.col_rpos()[mv.col_ptr()[kt] + colfill[kt]] = e;
           mv.col_ent()[mv.col_ptr()[kt] + colfill[kt]++] = entry_make(t, entry_kind(ent));
         }
       }
@@ -384,6 +387,12 @@ extern "C" int bd_tilemap_stats(const bd_problem* prob, int64_t* out) {
   out[2] = full;
   out[3] = part;
   return BD_OK;
+}
+
+extern "C" int64_t bd_tilemap_entries_bound(const bd_problem* prob) {
+  using namespace bd;
+  if (validate_problem(prob)) return -1;
+  return map_entries_bound(geom_of(*prob));
 }
 
 // Copies the host-built workspace image of the map (tests compare it with the

@@ -356,6 +356,14 @@ def tilemap_stats(prob: Problem):
     return {"tiles": out[0], "nonempty": out[1], "full": out[2], "partial": out[3]}
 
 
+def tilemap_entries_bound(prob: Problem) -> int:
+    p = prob.c()
+    n = _lib.lib().bd_tilemap_entries_bound(ctypes.byref(p))
+    if n < 0:
+        _err("invalid problem")
+    return int(n)
+
+
 def tilemap_host_image(prob: Problem):
     p = prob.c()
     L = _lib.lib()

@@ -1,8 +1,9 @@
 """The device tile-map builder (run inside every bd_attn_fwd / bd_attn_bwd call,
 map at workspace offset 0) writes exactly the host builder's image
 (bd_tilemap_host_image, itself bit-exact against the oracle's dense-mask
-classification in tests/test_tilemap_abi.py): header, both CSRs and both LPT
-orders, word for word (unused capacity words excluded)."""
+classification in tests/test_tilemap_abi.py): header, both CSRs, both LPT
+orders and the column-to-row-entry index, word for word (unused capacity words
+excluded)."""
 
 import pytest
 import torch
@@ -23,8 +24,9 @@ def _meaningful(img, NT, cap):
     ce = cp + NT + 1
     fo = ce + cap
     bo = fo + NT
+    cr = bo + NT
     return (img[:9], img[rp:rp + NT + 1], img[re:re + n], img[cp:cp + NT + 1], img[ce:ce + n],
-            img[fo:fo + NT], img[bo:bo + NT])
+            img[fo:fo + NT], img[bo:bo + NT], img[cr:cr + n])
 
 
 @pytest.mark.parametrize("P,R,B,rp,S", [
@@ -51,6 +53,6 @@ def test_device_map_equals_host_image(cuda_ok, P, R, B, rp, S):
     torch.cuda.synchronize()
     dev = ws[:4 * len(host)].view(torch.int32).cpu().tolist()
     NT, T0 = host[4], host[5]
-    cap = (len(host) - HDR - 2 * (NT + 1) - 2 * NT) // 2
+    cap = (len(host) - HDR - 2 * (NT + 1) - 2 * NT) // 3
     for a, b in zip(_meaningful(dev, NT, cap), _meaningful(host, NT, cap)):
         assert a == b

@@ -164,7 +164,7 @@ def test_row_length_within_capacity_stride_random():
             continue
         img = bd.ops.tilemap_host_image(bd.Problem(1, P, R, B, 1, 1, 64, repeat_prompt=rp, n_copies=S))
         NT, maxrow = img[4], img[7]
-        cap = (len(img) - 16 - 2 * (NT + 1) - 2 * NT) // 2
+        cap = (len(img) - 16 - 2 * (NT + 1) - 2 * NT) // 3
         assert maxrow <= cap // NT, (P, R, B, rp, S, maxrow, cap // NT)
 
 
@@ -188,3 +188,45 @@ def test_tilemap_varlen_sequences_vs_oracle_dense():
         got = bd.tilemap_dump(bd.Problem(1, cfg.prompt_len, R, cfg.block_size, 1, 1, 128))
         ref = tilemap.classify(OProblem(1, cfg.prompt_len, R, cfg.block_size, 1, 1, 128))
         assert got == ref, R
+
+
+def test_col_rpos_and_entries_bound():
+    """The map's column-to-row-entry index (where the dK/dV kernel stores a
+    tile's dS^T and the dQ kernel reads it, row by row): for every column entry
+    of k-tile kt naming q-tile t, row_ent[col_rpos] is kt and lies in row t's
+    range; every row entry is named exactly once.  And the O(NT) entry count
+    from the candidate ranges equals the builder's count (every candidate tile
+    is non-empty) on the BJ shapes and a randomised sweep of block sizes,
+    prompt lengths, modes and copies."""
+    import random
+    rng = random.Random(5)
+    cases = [(1024, 8192, 4, 1, 1), (512, 2048, 4, 1, 1), (1024, 8192, 4, 1, 4), (100, 300, 4, 0, 1),
+             (50, 334, 48, 0, 1), (36, 264, 12, 1, 3), (7, 121, 128, 1, 1), (42, 214, 8, 0, 2)]
+    for _ in range(150):
+        B = rng.choice([1, 2, 3, 4, 5, 7, 8, 12, 16, 32, 48, 64, 96, 128, 200, 300])
+        K = rng.randint(1, max(1, 1200 // B))
+        L = K * B
+        cases.append((rng.randint(0, L), 0, B, rng.randint(0, 1), rng.choice([1, 1, 2, 3])))
+        P = cases[-1][0]
+        cases[-1] = (P, L - P, B, cases[-1][3], cases[-1][4])
+    for P, R, B, rp, S in cases:
+        if R <= 0 or (P + R - (0 if rp else P)) <= 0:
+            continue
+        prob = bd.Problem(1, P, R, B, 1, 1, 64, repeat_prompt=rp, n_copies=S)
+        img = bd.ops.tilemap_host_image(prob)
+        NT, n = img[4], img[6]
+        cap = (len(img) - 16 - 2 * (NT + 1) - 2 * NT) // 3
+        rp_, re = 16, 16 + NT + 1
+        cp = re + cap
+        ce = cp + NT + 1
+        cr = ce + cap + 2 * NT
+        seen = [0] * n
+        for kt in range(NT):
+            for c in range(img[cp + kt], img[cp + kt + 1]):
+                t = img[ce + c] & 0x0FFFFFFF
+                e = img[cr + c]
+                assert img[rp_ + t] <= e < img[rp_ + t + 1], (P, R, B, rp, S, kt, t, e)
+                assert img[re + e] & 0x0FFFFFFF == kt
+                seen[e] += 1
+        assert seen == [1] * n
+        assert bd.ops.tilemap_entries_bound(prob) == n, (P, R, B, rp, S)
