@@ -1,7 +1,8 @@
 """Tiny end-to-end run of every ABI entry point, for compute-sanitizer
 (memcheck / racecheck / synccheck / initcheck): attention fwd + bwd (uniform,
 varlen, trace replay, d = 64, blocks not aligned to tiles, head-sharded
-strided slices, a small SDAR-8B-like slice), fused and two-pass logprob, DiPO, LM head fwd + bwd, decode
+strided slices, a small SDAR-8B-like slice, the opt-in stored-dS backward), fused (incl. the
+Qwen3-vocabulary register-tail variant) and two-pass logprob, DiPO, LM head fwd + bwd, decode
 attention + select.  Exits 0 when every call returned BD_OK."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -45,6 +46,18 @@ logp, lz = ops.logprob(z, t)
 w = torch.randn(64, device="cuda")
 ops.logprob_bwd(z, t, lz, w)
 ops.logprob(z.clone(), t, dlogp=w, dlogits=torch.empty_like(z))
+# the Qwen3 vocabulary: the fused kernel with register-held slice tails
+zq, tq = logits_inputs(8, 151936, seed=4)
+zq, tq = zq.cuda(), tq.cuda()
+ops.logprob(zq, tq, dlogp=torch.randn(8, device="cuda"), dlogits=torch.empty_like(zq))
+# the opt-in stored-dS backward, two chunks of one sequence
+cfg = base.with_(batch=2)
+prob = bd.Problem.from_cfg(cfg)
+os.environ["BD_BWD_DS"], os.environ["BD_BWD_DS_BUDGET_MB"] = "1", "1"
+q, k, v, do = [x.cuda() for x in attn_inputs(cfg)]
+o, lse = bd.attn_fwd(prob, q, k, v)
+bd.attn_bwd(prob, q, k, v, o, lse, do)
+os.environ["BD_BWD_DS"] = "0"
 rew = torch.tensor([1.0, 0.0], device="cuda")
 gid = torch.zeros(2, dtype=torch.int32, device="cuda")
 tl = torch.full((2,), 32, dtype=torch.int32, device="cuda")
