@@ -859,8 +859,13 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+#ifdef BD_DQ_T_TS  // timing-only: A from TMEM (garbage: the dQ columns), as if Q lived in TMEM
+          umma_ts(tbase + ((jg & 1) ? C::kColS1 : C::kColS0), tbase + C::kColDQ + k * 8,
+                  umma_desc_sw128(kaddr + off, 16, 1024), idesc_s, k > 0);
+#else
           umma_ss(tbase + ((jg & 1) ? C::kColS1 : C::kColS0), umma_desc_sw128(qaddr + off, 16, 1024),
                   umma_desc_sw128(kaddr + off, 16, 1024), idesc_s, k > 0);
+#endif
         }
         umma_commit(&s_full[jg & 1]);
       };
@@ -869,8 +874,13 @@ __global__ void __launch_bounds__(DqCfg<D>::kThreads, 1)
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+#ifdef BD_DQ_T_TS
+          umma_ts(tbase + C::kColDP, tbase + C::kColDQ + 64 + k * 8, umma_desc_sw128(vaddr + off, 16, 1024), idesc_s,
+                  k > 0);
+#else
           umma_ss(tbase + C::kColDP, umma_desc_sw128(doaddr + off, 16, 1024),
                   umma_desc_sw128(vaddr + off, 16, 1024), idesc_s, k > 0);
+#endif
         }
         umma_commit(dp_full);
         umma_commit(&kv_empty[slot(2 * jg + 1)]);  // V consumed
