@@ -215,3 +215,25 @@ def test_fused_logprob_target_positions(cuda_ok):
         assert metrics(d[i:i + 1], ref_dz[i:i + 1])["rel_l2"] <= DZ_REL_L2, i
         # the target entry itself: w (1 - p_t) within bf16 rounding
         assert abs(d[i, pos[i]] - ref_dz[i, pos[i]]) <= 1e-2 * abs(w[i].item()) + 1e-3, (i, d[i, pos[i]], ref_dz[i, pos[i]])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("V", [49120, 49152, 50176, 65536 + 32])
+def test_fused_logprob_register_tail_boundary(cuda_ok, V):
+    """Vocabularies at the fused kernel's register-tail threshold (a slice of
+    >= 6 x 256 16-byte vectors keeps 5 x 256 of them in registers): 49,152 is
+    the first size on the register path with ONE shared-memory vector per
+    thread; 49,120 the last without.  logp / LSE / dz vs the oracle."""
+    n = 5
+    z, t = logits_inputs(n, V, seed=V)
+    t[0] = V - 1
+    t[1] = 0
+    w = torch.randn(n, generator=torch.Generator().manual_seed(V), dtype=torch.float32)
+    logp, lse, dz = ops.logprob(z.cuda(), t.cuda(), dlogp=w.cuda())
+    torch.cuda.synchronize()
+    ref_lp, ref_lse = olp.logprob(z, t.long())
+    ref_dz = olp.logprob_grad(z, t.long(), w.double().numpy())
+    assert metrics(t2np(logp), ref_lp)["max_abs"] <= LOGP_MAX_ABS
+    assert metrics(t2np(lse), ref_lse)["max_abs"] <= LOGP_MAX_ABS
+    md = metrics(t2np(dz), ref_dz)
+    assert md["finite"] and md["rel_l2"] <= DZ_REL_L2, md
