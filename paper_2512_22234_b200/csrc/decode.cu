@@ -476,7 +476,14 @@ bool plan_decode(int batch, int B, int Hq, int Hkv, int cap, DecPlan& pl) {
   pl.nq = pl.hs * B <= 16 ? 16 : 32;
   const int units = batch * Hkv * pl.n_parts;
   const int tiles = (cap + kTile - 1) / kTile;
-  pl.n_splits = std::max(1, std::min(tiles, (8 * 148 + units - 1) / units));
+// Key splits only until ~4 CTAs per SM exist: each CTA's prologue (TMEM
+// alloc, barriers, Q load, ring fill) costs more than the tail imbalance
+// that finer splits would remove (SDAR-8B rollout, 128 x 8 kv heads: 4 per
+// SM -> no split, 0.478 ms; 8 -> 0.494; 16 -> 0.527; 32 -> 0.620).
+#ifndef BD_DEC_CTAS_PER_SM
+#define BD_DEC_CTAS_PER_SM 4
+#endif
+  pl.n_splits = std::max(1, std::min(tiles, (BD_DEC_CTAS_PER_SM * 148 + units - 1) / units));
   return true;
 }
 
