@@ -236,7 +236,10 @@ __global__ void __launch_bounds__(kThreads) logprob_bwd_kernel(int64_t n_rows, i
 // Measured (131,072 x 151,936): 12.0 ms standalone, 14.2-14.4 ms
 // inside the bench step, against 13.6 / 17.0 ms for the previous three-pass
 // kernel with a closing cluster barrier.
-constexpr int kCl = 4;
+#ifndef BD_LP_CLUSTER
+#define BD_LP_CLUSTER 4
+#endif
+constexpr int kCl = BD_LP_CLUSTER;
 #ifndef BD_LP_THREADS
 #define BD_LP_THREADS 256
 #endif
