@@ -111,14 +111,15 @@ int64_t bd_packed_len(const bd_problem* prob);
  * (backward = 1).  The forward workspace holds the tile map; the backward
  * one additionally holds D = rowsum(dO * O) and the log2-scaled LSE, fp32,
  * tile-major [b, Hq, n_tiles, 128], and -- for uniform (non-varlen) batches
- * -- when BD_BWD_DS=1 (env; off by default) the stored-dS buffer: bf16 dS^T
- * of every visible 128x128 tile of one chunk of sequences, Hq *
- * bd_tilemap_entries_bound(prob) * 32 KB per sequence, as many sequences
- * per chunk as fit BD_BWD_DS_BUDGET_MB (env, default 24,576 MiB; SDAR-8B:
- * 4 sequences, 22.3 GB).  Off, or one sequence over the budget: no buffer,
- * dQ recomputes S and dP.
- * The environment is read per call: keep it fixed between the workspace
- * query and the call.  Returns 0 for an invalid problem. */
+ * -- the stored-dS buffer: bf16 dS^T of every visible 128x128 tile of one
+ * chunk of sequences, Hq * bd_tilemap_entries_bound(prob) * 32 KB per
+ * sequence.  Env BD_BWD_DS unset: the buffer is used when the whole batch
+ * fits BD_BWD_DS_BUDGET_MB (default 8,192 MiB; e.g. SDAR-1.7B at batch 16:
+ * 3.6 GB; SDAR-8B: no buffer); BD_BWD_DS=1: always, in chunks of as many
+ * sequences as fit the budget (default 24,576 MiB; SDAR-8B: 4 sequences,
+ * 22.3 GB); BD_BWD_DS=0: never.  Without the buffer dQ recomputes S and dP.
+ * The environment is read per call: keep it fixed between this query and
+ * the call.  Returns 0 for an invalid problem. */
 size_t bd_attn_workspace_bytes(const bd_problem* prob, int backward);
 
 /* Forward.
@@ -139,7 +140,7 @@ int bd_attn_fwd(const bd_problem* prob, const void* q, const void* k, const void
  * and dv sum over the Hq/Hkv query heads of each kv head.  ws must be
  * >= bd_attn_workspace_bytes(prob, 1) bytes.  Kernels: preprocess, dK/dV
  * over the column tile map, dQ over the row tile map (recomputing S and dP).
- * With the stored-dS buffer (BD_BWD_DS=1, see bd_attn_workspace_bytes), per
+ * With the stored-dS buffer (see bd_attn_workspace_bytes), per
  * chunk of sequences the dK/dV kernel also stores each tile's dS^T = P (dP -
  * D), bf16 (the value its dK MMA consumes), and dQ = scale dS K reads it back
  * instead of recomputing.  No atomics: the result is deterministic. */

@@ -36,10 +36,11 @@ struct DsPlan {
   int chunk = 0;
 };
 // The plan's sizes for a problem (host, deterministic): bytes of the dS^T
-// buffer (0 = path off).  BD_BWD_DS=1 enables the path; BD_BWD_DS_BUDGET_MB
-// (default 24,576) caps the buffer, which then holds floor(budget / per
-// sequence) sequences (off if one sequence exceeds it).  Opt-in: BD_BWD_DS=1
-// (measured no faster than the recompute path on B200).
+// buffer (0 = path off).  BD_BWD_DS unset: on when the whole batch fits one
+// chunk of BD_BWD_DS_BUDGET_MB (default 8,192); BD_BWD_DS=1: on, chunked
+// (floor(budget / per sequence) sequences per chunk, default budget 24,576;
+// off if one sequence exceeds it); BD_BWD_DS=0: off.  The environment is
+// read per call: keep it fixed between the workspace query and the call.
 size_t ds_plan_bytes(const bd_problem& p, const Geom& g, long long* stride, int* chunk);
 int run_attn_bwd(const bd_problem& p, const Geom& g, const void* q, const void* k, const void* v, const void* o,
                  const float* lse, const void* dout, void* dq, void* dk, void* dv, const int* map, int map_stride,

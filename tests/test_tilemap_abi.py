@@ -128,8 +128,9 @@ def test_row_and_key_intervals_agree(P, R, B, rp):
     assert n.value == 0
 
 
-def test_varlen_validation_and_workspace():
+def test_varlen_validation_and_workspace(monkeypatch):
     """Per-sequence lengths are checked on the host (S:214 layout errors)."""
+    monkeypatch.setenv("BD_BWD_DS", "0")  # compare map / vector space only (no stored-dS buffer)
     L = _lib.lib()
     ok = bd.Problem(3, 64, 320, 4, 4, 2, 128, seq_prompt_lens=(64, 32, 0), seq_response_lens=(320, 96, 200))
     assert bd.packed_len(ok) == 2 * 384
