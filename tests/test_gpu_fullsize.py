@@ -41,8 +41,15 @@ def _slice(x, b, h):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["sdar_1_7b", "sdar_8b", "sweep_b8", "sweep_b32", "trace_s4"])
-def test_fullsize_sampled_parity(cuda_ok, name):
+@pytest.mark.parametrize("name,ds", [("sdar_1_7b", None), ("sdar_8b", None), ("sweep_b8", None),
+                                     ("sweep_b32", None), ("trace_s4", None),
+                                     # the stored-dS backward forced on, chunked (SDAR-8B: 4
+                                     # sequences per 22.3 GB chunk; sweep: 2 chunks); under the
+                                     # default policy SDAR-1.7B already takes it, SDAR-8B does not
+                                     ("sdar_8b", "1"), ("sweep_b8", "1")])
+def test_fullsize_sampled_parity(cuda_ok, name, ds, monkeypatch):
+    if ds is not None:
+        monkeypatch.setenv("BD_BWD_DS", ds)
     cfg = CONFIGS[name]
     prob = bd.Problem.from_cfg(cfg)
     q, k, v, do = attn_inputs(cfg, device="cuda")
