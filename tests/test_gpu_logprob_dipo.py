@@ -237,3 +237,26 @@ def test_fused_logprob_register_tail_boundary(cuda_ok, V):
     assert metrics(t2np(lse), ref_lse)["max_abs"] <= LOGP_MAX_ABS
     md = metrics(t2np(dz), ref_dz)
     assert md["finite"] and md["rel_l2"] <= DZ_REL_L2, md
+
+
+@pytest.mark.gpu
+def test_fused_logprob_in_place_qwen3(cuda_ok):
+    """The fused kernel in place (dlogits = logits) at the Qwen3 vocabulary --
+    the bench's and a training step's use: each CTA reads its slice (shared
+    memory part by bulk copy, register tail by streaming loads) before writing
+    dz over it; a wide-spread row takes the global-memory redo path, which must
+    still see the original logits.  Bit-identical to the out-of-place call."""
+    n, V = 6, VOCAB_QWEN3
+    z, t = logits_inputs(n, V, seed=55)
+    z[0, :2048] = -60.0  # the redo path (first vectors far below the rest)
+    w = torch.randn(n, generator=torch.Generator().manual_seed(3), dtype=torch.float32)
+    zc, tc, wc = z.cuda(), t.cuda(), w.cuda()
+    lp1, ls1, dz1 = ops.logprob(zc, tc, dlogp=wc)
+    zi = zc.clone()
+    lp2, ls2, dz2 = ops.logprob(zi, tc, dlogp=wc, dlogits=zi)
+    torch.cuda.synchronize()
+    assert dz2.data_ptr() == zi.data_ptr()
+    assert torch.equal(lp1, lp2) and torch.equal(ls1, ls2)
+    assert torch.equal(dz1.view(torch.int16), zi.view(torch.int16))
+    ref_dz = olp.logprob_grad(z, t.long(), w.double().numpy())
+    assert metrics(t2np(zi), ref_dz)["rel_l2"] <= DZ_REL_L2
